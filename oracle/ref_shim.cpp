@@ -1,0 +1,399 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A C-ABI shim over the UNMODIFIED reference headers, compiled in place from
+// /root/reference/proj/include by oracle/Makefile into oracle/_ref/ (never
+// copied into this repo).  It lets the Python tests and bench.py's reference
+// arm call the reference's own spmm_local / spgemm_local / csr_add /
+// generators / run_multiply (reference: proj/include/rdmm/{tile,gen,algos}.hpp)
+// on caller-owned host buffers.
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <thread>
+
+#include "rdmm/algos.hpp"
+#include "rdmm/gen.hpp"
+#include "rdmm_oracle.h"  // orc_csr layout only
+
+using namespace rdmm;
+
+namespace {
+
+template <typename T>
+CsrView<T> view(const orc_csr* a) {
+  CsrView<T> v;
+  v.rows = a->rows;
+  v.cols = a->cols;
+  v.row_ptr = a->row_ptr;
+  v.col_idx = a->col_idx;
+  v.values = static_cast<const T*>(a->values);
+  return v;
+}
+
+template <typename T>
+CsrTile<T> tile_of(const orc_csr* a) {
+  CsrTile<T> t(a->rows, a->cols);
+  t.row_ptr.assign(a->row_ptr, a->row_ptr + a->rows + 1);
+  t.col_idx.assign(a->col_idx, a->col_idx + a->nnz);
+  const T* v = static_cast<const T*>(a->values);
+  t.values.assign(v, v + a->nnz);
+  return t;
+}
+
+template <typename T>
+void export_csr(const CsrTile<T>& t, orc_csr* out) {
+  out->rows = t.rows;
+  out->cols = t.cols;
+  out->nnz = t.nnz();
+  out->dtype = sizeof(T);
+  out->row_ptr = static_cast<uint32_t*>(std::malloc((t.rows + 1) * 4));
+  out->col_idx = static_cast<uint32_t*>(std::malloc(t.nnz() * 4 + 4));
+  out->values = std::malloc(t.nnz() * sizeof(T) + 8);
+  std::memcpy(out->row_ptr, t.row_ptr.data(), (t.rows + 1) * 4);
+  std::memcpy(out->col_idx, t.col_idx.data(), t.nnz() * 4);
+  std::memcpy(out->values, t.values.data(), t.nnz() * sizeof(T));
+}
+
+int code_of(const std::exception_ptr& e) {
+  try {
+    std::rethrow_exception(e);
+  } catch (const dimension_error&) {
+    return -1;
+  } catch (const protocol_error&) {
+    return -4;
+  } catch (const heap_exhausted_error&) {
+    return -5;
+  } catch (const queue_full_error&) {
+    return -6;
+  } catch (const fabric_error&) {
+    return -3;
+  } catch (const std::invalid_argument&) {
+    return -1;
+  } catch (...) {
+    return -9;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+struct ref_report {
+  double wall_seconds;
+  double max_total_seconds;
+  double checksum;
+  uint64_t total_flops;
+  uint64_t total_multiplies;
+  uint64_t total_steals;
+  uint64_t nranks;
+  uint64_t multiplies[64];
+  uint64_t flops[64];
+  uint64_t steals[64];
+  uint64_t steals_local[64];
+  uint64_t pushes[64];
+  uint64_t pops[64];
+  double total_seconds[64];
+};
+
+uint64_t ref_splitmix64(uint64_t x) { return rng::splitmix64(x); }
+uint64_t ref_rng_at(uint64_t s, uint64_t c) { return rng::at(s, c); }
+unsigned ref_hardware_concurrency() { return std::thread::hardware_concurrency(); }
+
+int ref_rmat(double a, double b, double c, double d, uint32_t scale,
+             uint32_t ef, uint64_t seed, int mult, int dtype, orc_csr* out) {
+  try {
+    RmatParams p;
+    p.a = a;
+    p.b = b;
+    p.c = c;
+    p.d = d;
+    p.scale = scale;
+    p.edgefactor = ef;
+    p.seed = seed;
+    DupPolicy dp = mult ? DupPolicy::multiplicity : DupPolicy::collapse_to_one;
+    if (dtype == 8)
+      export_csr(rmat<double>(p, dp), out);
+    else
+      export_csr(rmat<float>(p, dp), out);
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+int ref_uniform_tiles(uint64_t m, uint64_t k, uint32_t p, double d,
+                      uint64_t seed, int dtype, orc_csr* out) {
+  try {
+    if (dtype == 8)
+      export_csr(uniform_tiles<double>(m, k, p, d, seed), out);
+    else
+      export_csr(uniform_tiles<float>(m, k, p, d, seed), out);
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+int ref_random_csr(uint32_t rows, uint32_t cols, double density, uint64_t seed,
+                   int max_value, int dtype, orc_csr* out) {
+  if (dtype == 8)
+    export_csr(random_csr<double>(rows, cols, density, seed, max_value), out);
+  else
+    export_csr(random_csr<float>(rows, cols, density, seed, max_value), out);
+  return 0;
+}
+
+int ref_permute_symmetric(const orc_csr* m, uint64_t seed, orc_csr* out) {
+  try {
+    if (m->dtype == 8)
+      export_csr(permute_symmetric(tile_of<double>(m), seed), out);
+    else
+      export_csr(permute_symmetric(tile_of<float>(m), seed), out);
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+void ref_random_dense(uint32_t rows, uint32_t cols, uint64_t seed,
+                      int max_value, int dtype, void* out) {
+  if (dtype == 8) {
+    auto t = random_dense<double>(rows, cols, seed, max_value);
+    std::memcpy(out, t.values.data(), t.values.size() * 8);
+  } else {
+    auto t = random_dense<float>(rows, cols, seed, max_value);
+    std::memcpy(out, t.values.data(), t.values.size() * 4);
+  }
+}
+
+// c += a*b on caller buffers (views, no copies): tile.hpp:170-188.
+int ref_spmm_local(const orc_csr* a, uint32_t b_rows, uint32_t n,
+                   const void* b, void* c, uint64_t* flops) {
+  try {
+    FlopMeter m;
+    if (a->dtype == 8) {
+      DenseConstView<double> bv;
+      bv.rows = b_rows;
+      bv.cols = n;
+      bv.values = static_cast<const double*>(b);
+      DenseView<double> cv;
+      cv.rows = a->rows;
+      cv.cols = n;
+      cv.values = static_cast<double*>(c);
+      m = spmm_local(view<double>(a), bv, cv);
+    } else {
+      DenseConstView<float> bv;
+      bv.rows = b_rows;
+      bv.cols = n;
+      bv.values = static_cast<const float*>(b);
+      DenseView<float> cv;
+      cv.rows = a->rows;
+      cv.cols = n;
+      cv.values = static_cast<float*>(c);
+      m = spmm_local(view<float>(a), bv, cv);
+    }
+    if (flops) *flops = m.flops;
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+int ref_spgemm_local(const orc_csr* a, const orc_csr* b, orc_csr* out,
+                     uint64_t* flops) {
+  try {
+    if (a->dtype == 8) {
+      auto [c, m] = spgemm_local(view<double>(a), view<double>(b));
+      export_csr(c, out);
+      if (flops) *flops = m.flops;
+    } else {
+      auto [c, m] = spgemm_local(view<float>(a), view<float>(b));
+      export_csr(c, out);
+      if (flops) *flops = m.flops;
+    }
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+uint64_t ref_spgemm_flops(const orc_csr* a, const orc_csr* b) {
+  return a->dtype == 8 ? spgemm_flops(view<double>(a), view<double>(b))
+                       : spgemm_flops(view<float>(a), view<float>(b));
+}
+
+int ref_csr_add(const orc_csr* a, const orc_csr* b, orc_csr* out) {
+  try {
+    if (a->dtype == 8)
+      export_csr(csr_add(view<double>(a), view<double>(b)), out);
+    else
+      export_csr(csr_add(view<float>(a), view<float>(b)), out);
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+void ref_csr_free(orc_csr* a) {
+  std::free(a->row_ptr);
+  std::free(a->col_idx);
+  std::free(a->values);
+}
+
+}  // extern "C"
+
+namespace {
+
+RunOptions make_opts(int variant, int ws_base, int prefetch, int offset,
+                     uint64_t seed, double delay_ns_per_flop,
+                     double random_delay_ms) {
+  RunOptions o;
+  o.variant = static_cast<Variant>(variant);
+  o.ws_base = static_cast<Variant>(ws_base);
+  o.prefetch = prefetch != 0;
+  o.offset = offset != 0;
+  o.seed = seed;
+  o.delay_ns_per_flop = delay_ns_per_flop;
+  o.random_delay_ms_max = random_delay_ms;
+  o.record_events = true;
+  o.record_triples = false;
+  return o;
+}
+
+void fill_report(const RunReport& r, ref_report* rep) {
+  std::memset(rep, 0, sizeof(*rep));
+  rep->wall_seconds = r.wall_seconds;
+  rep->checksum = r.checksum;
+  rep->total_flops = r.total_flops();
+  rep->total_multiplies = r.total_multiplies();
+  rep->total_steals = r.total_steals();
+  rep->nranks = r.per_rank.size();
+  for (std::size_t p = 0; p < r.per_rank.size() && p < 64; ++p) {
+    const auto& s = r.per_rank[p];
+    rep->multiplies[p] = s.multiplies;
+    rep->flops[p] = s.meter.flops;
+    rep->steals[p] = s.steals;
+    rep->steals_local[p] = s.steals_with_local_component;
+    rep->pushes[p] = s.queue_pushes;
+    rep->pops[p] = s.queue_pops;
+    rep->total_seconds[p] = s.total_seconds;
+    if (s.total_seconds > rep->max_total_seconds)
+      rep->max_total_seconds = s.total_seconds;
+  }
+}
+
+template <typename T>
+int run_spmm(const RunOptions& o, uint32_t pr, uint32_t pc, uint64_t m,
+             uint64_t k, uint64_t n, uint32_t tm, uint32_t tk, uint32_t tn,
+             const orc_csr* a, const void* b, void* c, uint64_t heap_bytes,
+             ref_report* rep) {
+  const uint32_t P = pr * pc;
+  if (heap_bytes == 0) {
+    uint64_t bytes = a->nnz * (4 + sizeof(T)) + (a->rows + 1) * 4ull * 8 +
+                     (k * n + 2 * m * n) * sizeof(T);
+    heap_bytes = 3 * bytes / P + (tm * uint64_t(tn) * sizeof(T) + 64) * 64 +
+                 (16ull << 20);
+  }
+  FabricConfig cfg;
+  cfg.nranks = P;
+  cfg.heap_bytes = heap_bytes;
+  Fabric f(cfg);
+  ProcGrid g{pr, pc};
+  DistSparse<T> A(f, m, k, tm, tk, g, 0);
+  DistDense<T> B(f, k, n, tk, tn, g, 1);
+  DistDense<T> C(f, m, n, tm, tn, g, 2);
+  CsrTile<T> ga = tile_of<T>(a);
+  std::vector<T> gb(static_cast<const T*>(b), static_cast<const T*>(b) + k * n);
+  std::vector<T> gc(static_cast<T*>(c), static_cast<T*>(c) + m * n);
+  run_ranks(f, [&](RankCtx& ctx) {
+    A.init_from_global(ctx, ga);
+    B.init_from_global(ctx, gb);
+    C.init_from_global(ctx, gc);
+  });
+  RunReport r = run_multiply(f, A, B, C, o);
+  auto out = C.to_global();
+  std::memcpy(c, out.data(), out.size() * sizeof(T));
+  fill_report(r, rep);
+  return 0;
+}
+
+template <typename T>
+int run_spgemm(const RunOptions& o, uint32_t pr, uint32_t pc, uint64_t m,
+               uint64_t k, uint64_t n, uint32_t tm, uint32_t tk, uint32_t tn,
+               const orc_csr* a, const orc_csr* b, const orc_csr* c0,
+               orc_csr* out, uint64_t heap_bytes, ref_report* rep) {
+  const uint32_t P = pr * pc;
+  if (heap_bytes == 0) {
+    uint64_t fl = spgemm_flops(view<T>(a), view<T>(b)) / 2;
+    uint64_t bytes = (a->nnz + b->nnz + c0->nnz + 2 * fl) * (4 + sizeof(T)) +
+                     (m + k + 2) * 4ull * 16;
+    heap_bytes = 4 * bytes / P + (16ull << 20);
+  }
+  FabricConfig cfg;
+  cfg.nranks = P;
+  cfg.heap_bytes = heap_bytes;
+  Fabric f(cfg);
+  ProcGrid g{pr, pc};
+  DistSparse<T> A(f, m, k, tm, tk, g, 0);
+  DistSparse<T> B(f, k, n, tk, tn, g, 1);
+  DistSparse<T> C(f, m, n, tm, tn, g, 2);
+  CsrTile<T> ga = tile_of<T>(a), gb = tile_of<T>(b), gc = tile_of<T>(c0);
+  run_ranks(f, [&](RankCtx& ctx) {
+    A.init_from_global(ctx, ga);
+    B.init_from_global(ctx, gb);
+    C.init_from_global(ctx, gc);
+  });
+  RunReport r = run_multiply(f, A, B, C, o);
+  export_csr(C.to_global(), out);
+  fill_report(r, rep);
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+// run_multiply (algos.hpp:673-752) for SpMM with host-global inputs; c holds
+// C0 on entry and the result on return.
+int ref_run_multiply_spmm(int dtype, int variant, int ws_base, int prefetch,
+                          int offset, uint64_t seed, double delay_ns_per_flop,
+                          double random_delay_ms, uint32_t pr, uint32_t pc,
+                          uint64_t m, uint64_t k, uint64_t n, uint32_t tm,
+                          uint32_t tk, uint32_t tn, const orc_csr* a,
+                          const void* b, void* c, uint64_t heap_bytes,
+                          ref_report* rep) {
+  try {
+    RunOptions o = make_opts(variant, ws_base, prefetch, offset, seed,
+                             delay_ns_per_flop, random_delay_ms);
+    if (dtype == 8)
+      return run_spmm<double>(o, pr, pc, m, k, n, tm, tk, tn, a, b, c,
+                              heap_bytes, rep);
+    return run_spmm<float>(o, pr, pc, m, k, n, tm, tk, tn, a, b, c,
+                           heap_bytes, rep);
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+int ref_run_multiply_spgemm(int dtype, int variant, int ws_base, int prefetch,
+                            int offset, uint64_t seed, double delay_ns_per_flop,
+                            double random_delay_ms, uint32_t pr, uint32_t pc,
+                            uint64_t m, uint64_t k, uint64_t n, uint32_t tm,
+                            uint32_t tk, uint32_t tn, const orc_csr* a,
+                            const orc_csr* b, const orc_csr* c0, orc_csr* out,
+                            uint64_t heap_bytes, ref_report* rep) {
+  try {
+    RunOptions o = make_opts(variant, ws_base, prefetch, offset, seed,
+                             delay_ns_per_flop, random_delay_ms);
+    if (dtype == 8)
+      return run_spgemm<double>(o, pr, pc, m, k, n, tm, tk, tn, a, b, c0, out,
+                                heap_bytes, rep);
+    return run_spgemm<float>(o, pr, pc, m, k, n, tm, tk, tn, a, b, c0, out,
+                             heap_bytes, rep);
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+}  // extern "C"
