@@ -1,0 +1,32 @@
+# Top-level build: the B200 C-ABI library and the C++ host library.
+#   make            -> paper_2311_18141_b200/lib/librdmm_cuda.so (+ oracle)
+# All device code is compiled for sm_100a only.
+NVCC    ?= /usr/local/cuda/bin/nvcc
+PKG     := paper_2311_18141_b200
+SRC     := $(PKG)/csrc
+OBJ     := build/obj
+LIBDIR  := $(PKG)/lib
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 \
+           -Iinclude -I$(SRC) --expt-relaxed-constexpr -Xptxas -warn-spills
+CUDA_SRCS := $(wildcard $(SRC)/*.cu)
+CUDA_OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CUDA_SRCS))
+HDRS := $(wildcard include/*.h) $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.h)
+
+all: $(LIBDIR)/librdmm_cuda.so oracle
+
+$(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIBDIR)/librdmm_cuda.so: $(CUDA_OBJS)
+	@mkdir -p $(LIBDIR)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(CUDA_OBJS) -lpthread -lrt -ldl
+
+oracle:
+	$(MAKE) -s -C oracle
+
+clean:
+	rm -rf build $(LIBDIR)
+
+.PHONY: all oracle clean

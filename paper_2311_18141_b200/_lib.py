@@ -1,0 +1,105 @@
+"""ctypes binding of the C-ABI (include/rdmm_cuda.h) -- the reference-facing
+boundary of the B200 path.
+
+The library is built in-tree (``make`` / ``__graft_entry__.build()``) into
+``paper_2311_18141_b200/lib/librdmm_cuda.so``.  There is no fallback: if the
+shared object is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "librdmm_cuda.so")
+
+
+class RdmmError(RuntimeError):
+    code = -1
+
+
+class DimensionError(RdmmError):  # tile.hpp:19-23
+    code = 1
+
+
+class FabricError(RdmmError):  # fabric.hpp:38-41
+    code = 2
+
+
+class HeapExhaustedError(FabricError):  # fabric.hpp:43-53
+    code = 3
+
+
+class QueueFullError(FabricError):  # fabric.hpp:55-60
+    code = 4
+
+
+class ProtocolError(FabricError):  # algos.hpp:98-101
+    code = 5
+
+
+class CudaError(RdmmError):
+    code = 6
+
+
+class InvalidArgument(RdmmError, ValueError):
+    code = 7
+
+
+_ERRORS = {c.code: c for c in (DimensionError, FabricError, HeapExhaustedError,
+                               QueueFullError, ProtocolError, CudaError, InvalidArgument)}
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build the CUDA extension first "
+            "(python -c 'import __graft_entry__ as g; g.build()' or `make`). "
+            "There is no CPU fallback.")
+    return C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+
+
+lib = _load()
+
+u32, u64, i32, i64 = C.c_uint32, C.c_uint64, C.c_int32, C.c_int64
+vp, sz, dbl, cint = C.c_void_p, C.c_size_t, C.c_double, C.c_int
+P = C.POINTER
+
+
+def _fn(name, args, res=cint):
+    f = getattr(lib, name)
+    f.argtypes = args
+    f.restype = res
+    return f
+
+
+rdmm_last_error = _fn("rdmm_last_error", [], C.c_char_p)
+rdmm_version = _fn("rdmm_version", [], C.c_char_p)
+rdmm_spmm_workspace_bytes = _fn("rdmm_spmm_workspace_bytes", [u32, u64, u32, cint], sz)
+_spmm_args = [u32, u32, u32, u64, vp, vp, vp, vp, u64, vp, u64, vp, sz, vp, P(u64)]
+rdmm_spmm_csr_f32 = _fn("rdmm_spmm_csr_f32", _spmm_args)
+rdmm_spmm_csr_f64 = _fn("rdmm_spmm_csr_f64", _spmm_args)
+rdmm_dense_add_into_f32 = _fn("rdmm_dense_add_into_f32", [u32, u32, vp, u64, vp, u64, vp])
+rdmm_dense_add_into_f64 = _fn("rdmm_dense_add_into_f64", [u32, u32, vp, u64, vp, u64, vp])
+rdmm_gen_rng_at = _fn("rdmm_gen_rng_at", [u64, u64, u64, vp, vp])
+rdmm_gen_random_dense = _fn("rdmm_gen_random_dense", [u64, u64, cint, cint, vp, vp])
+rdmm_gen_real_twin = _fn("rdmm_gen_real_twin", [u64, u64, cint, vp, vp])
+rdmm_gen_rmat_begin = _fn("rdmm_gen_rmat_begin",
+                          [dbl, dbl, dbl, dbl, u32, u32, u64, cint, P(vp), P(u64)])
+rdmm_gen_uniform_tiles_begin = _fn("rdmm_gen_uniform_tiles_begin",
+                                   [u64, u64, u32, dbl, u64, P(vp), P(u64)])
+rdmm_gen_finish = _fn("rdmm_gen_finish", [vp, cint, vp, vp, vp])
+rdmm_gen_abort = _fn("rdmm_gen_abort", [vp], None)
+
+
+def check(rc: int, what: str = "") -> None:
+    """Raise the exception mirroring the reference taxonomy for status rc."""
+    if rc == 0:
+        return
+    msg = (rdmm_last_error() or b"").decode(errors="replace")
+    cls = _ERRORS.get(rc, RdmmError)
+    raise cls(f"{what}: {msg}" if what else msg)
+
+
+def loaded_path() -> str:
+    return LIB_PATH

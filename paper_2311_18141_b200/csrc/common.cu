@@ -1,0 +1,67 @@
+// common.cu -- error plumbing and per-thread scratch for the C-ABI.
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace rdmm_impl {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+namespace {
+struct Scratch {
+  struct Buf {
+    void* p = nullptr;
+    size_t n = 0;
+  };
+  // [device][slot]
+  std::vector<std::vector<Buf>> bufs;
+  ~Scratch() {
+    // Process teardown: the CUDA context may already be gone; leak quietly.
+  }
+};
+thread_local Scratch g_scratch;
+}  // namespace
+
+void* scratch(size_t bytes, int slot) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  auto& per = g_scratch.bufs;
+  if (per.size() <= size_t(dev)) per.resize(dev + 1);
+  auto& slots = per[dev];
+  if (slots.size() <= size_t(slot)) slots.resize(slot + 1);
+  auto& b = slots[slot];
+  if (b.n >= bytes) return b.p;
+  if (b.p) {
+    cudaDeviceSynchronize();  // in-flight kernels may still use the old one
+    cudaFree(b.p);
+    b.p = nullptr;
+    b.n = 0;
+  }
+  size_t n = bytes + bytes / 4 + 4096;
+  if (cudaMalloc(&b.p, n) != cudaSuccess) {
+    cudaGetLastError();
+    b.p = nullptr;
+    return nullptr;
+  }
+  b.n = n;
+  return b.p;
+}
+
+}  // namespace rdmm_impl
+
+extern "C" const char* rdmm_last_error(void) {
+  return rdmm_impl::g_last_error.c_str();
+}
+
+extern "C" const char* rdmm_version(void) {
+  return "rdmm-b200 0.1 (sm_100a)";
+}

@@ -1,0 +1,50 @@
+// common.cuh -- shared helpers for the sm_100a kernels and the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "rdmm_cuda.h"
+
+namespace rdmm_impl {
+
+// Thread-local last error (rdmm_last_error); set by every failing entry point.
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+#define RDMM_CUDA_TRY(expr)                                                \
+  do {                                                                     \
+    cudaError_t e_ = (expr);                                               \
+    if (e_ != cudaSuccess)                                                 \
+      return ::rdmm_impl::fail(RDMM_ERR_CUDA, std::string(#expr ": ") +    \
+                                                  cudaGetErrorString(e_)); \
+  } while (0)
+
+inline cudaStream_t as_stream(rdmm_stream_t s) {
+  return reinterpret_cast<cudaStream_t>(s);
+}
+
+inline int num_sms() {
+  static thread_local int dev_cached = -1, sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != dev_cached) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    dev_cached = dev;
+  }
+  return sms;
+}
+
+// Grow-only per-(thread, device) scratch used when the caller passes no
+// workspace.  Stream-ordered reuse: callers on one host thread serialise
+// their kernels on one stream per device (the algorithms in this library do).
+void* scratch(size_t bytes, int slot = 0);
+
+__host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) {
+  return (a + b - 1) / b;
+}
+
+}  // namespace rdmm_impl

@@ -1,0 +1,428 @@
+// spmm.cu -- C += A*B for CSR A and row-major tall-skinny B on sm_100a.
+//
+// Reference: spmm_local, /root/reference/proj/include/rdmm/tile.hpp:170-188
+// (scalar triple loop, one B-row gather per nonzero, k ascending).
+//
+// B200 design (memory-bound, CUDA cores):
+//  * nnz-balanced chunks.  The nonzeros are cut into `nchunks` equal ranges
+//    of Q; a worker (a group of G lanes) owns whole chunks, so hub rows of
+//    R-MAT (32K nnz at scale 22) are spread over many workers and 41% empty
+//    rows cost nothing.  A row wholly inside a chunk is accumulated in the
+//    reference order starting from C (fma chain) and stored once -> bitwise
+//    equal to the reference for any values.  A row cut by chunk boundaries
+//    leaves per-chunk partials (the first one seeded with C); a fix-up pass
+//    adds them in ascending chunk order -> deterministic.
+//  * One 512-B row of B per nonzero is gathered as 32 lanes x 16 B
+//    (float4 / double2) through the read-only path, U=8 gathers in flight per
+//    worker before the fused multiply-adds.
+//  * col_idx/val are read 32 at a time (one coalesced load per lane) and
+//    broadcast with shuffles.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace rdmm_impl {
+namespace {
+
+template <typename T, int VEC>
+struct VecOf;
+template <>
+struct VecOf<float, 4> {
+  using type = float4;
+};
+template <>
+struct VecOf<double, 2> {
+  using type = double2;
+};
+template <>
+struct VecOf<float, 1> {
+  using type = float;
+};
+template <>
+struct VecOf<double, 1> {
+  using type = double;
+};
+
+__device__ __forceinline__ float4 vfma(float a, float4 b, float4 c) {
+  return make_float4(fmaf(a, b.x, c.x), fmaf(a, b.y, c.y), fmaf(a, b.z, c.z),
+                     fmaf(a, b.w, c.w));
+}
+__device__ __forceinline__ double2 vfma(double a, double2 b, double2 c) {
+  return make_double2(fma(a, b.x, c.x), fma(a, b.y, c.y));
+}
+__device__ __forceinline__ float vfma(float a, float b, float c) {
+  return fmaf(a, b, c);
+}
+__device__ __forceinline__ double vfma(double a, double b, double c) {
+  return fma(a, b, c);
+}
+__device__ __forceinline__ float4 vadd(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ double2 vadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ float vadd(float a, float b) { return a + b; }
+__device__ __forceinline__ double vadd(double a, double b) { return a + b; }
+__device__ __forceinline__ uint64_t umin(uint64_t a, uint64_t b) {
+  return a < b ? a : b;
+}
+__device__ __forceinline__ uint64_t umax(uint64_t a, uint64_t b) {
+  return a > b ? a : b;
+}
+template <typename V>
+__device__ __forceinline__ V vzero() {
+  V v;
+  memset(&v, 0, sizeof(V));
+  return v;
+}
+
+template <typename T>
+struct SpmmArgs {
+  const uint32_t* __restrict__ rp;
+  const uint32_t* __restrict__ ci;
+  const T* __restrict__ val;
+  const T* __restrict__ B;
+  T* __restrict__ C;
+  T* __restrict__ head_val;  // [nchunks][wstride]
+  T* __restrict__ tail_val;  // [nchunks][wstride]
+  int32_t* __restrict__ tail_row;  // [nchunks]
+  uint64_t ldb, ldc;
+  uint64_t nnz, Q;
+  uint32_t rows, nvec, nchunks, wstride;
+};
+
+template <int G>
+__device__ __forceinline__ unsigned group_mask() {
+  if constexpr (G == 32) {
+    return 0xffffffffu;
+  } else {
+    const unsigned lane = threadIdx.x & 31u;
+    return ((1u << G) - 1u) << (lane / G * G);
+  }
+}
+
+constexpr int kThreads = 256;
+constexpr int kWin = 32;  // nonzeros staged per window
+constexpr int kU = 8;     // B-row gathers in flight per worker
+
+template <typename T, int VEC, int G, int NV>
+__global__ void __launch_bounds__(kThreads)
+    spmm_chunks(const SpmmArgs<T> p) {
+  using V = typename VecOf<T, VEC>::type;
+  constexpr int SL = kWin / G;  // staged entries per lane
+  const unsigned gm = group_mask<G>();
+  const uint32_t lane = threadIdx.x % G;
+  const uint32_t worker = (blockIdx.x * kThreads + threadIdx.x) / G;
+  const uint32_t nworkers = gridDim.x * (kThreads / G);
+  const V* __restrict__ Bv = reinterpret_cast<const V*>(p.B);
+  V* __restrict__ Cv = reinterpret_cast<V*>(p.C);
+  const uint64_t ldbv = p.ldb / VEC, ldcv = p.ldc / VEC;
+  bool colok[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) colok[v] = lane + G * v < p.nvec;
+
+  for (uint32_t c = worker; c < p.nchunks; c += nworkers) {
+    const uint64_t lo = uint64_t(c) * p.Q;
+    const uint64_t hi = umin(lo + p.Q, p.nnz);
+    // row containing nonzero `lo`: largest r with rp[r] <= lo
+    uint32_t l = 0, h = p.rows;
+    while (h - l > 1) {
+      uint32_t m = (l + h) >> 1;
+      if (__ldg(p.rp + m) <= lo)
+        l = m;
+      else
+        h = m;
+    }
+    uint32_t r = l;
+    uint32_t rs = __ldg(p.rp + r);
+    uint32_t re = __ldg(p.rp + r + 1);
+    int32_t trow = -1;
+    while (rs < hi) {
+      const uint32_t re_next = (r + 2 <= p.rows) ? __ldg(p.rp + r + 2) : re;
+      const uint64_t s = umax(rs, lo), e = umin(re, hi);
+      if (s < e) {
+        const bool starts = rs >= lo, ends = re <= hi;
+        V acc[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+          acc[v] = (starts && colok[v]) ? Cv[uint64_t(r) * ldcv + lane + G * v]
+                                        : vzero<V>();
+        for (uint64_t base = s; base < e; base += kWin) {
+          const uint32_t cnt = uint32_t(umin(kWin, e - base));
+          uint32_t kk[SL];
+          T aa[SL];
+#pragma unroll
+          for (int j = 0; j < SL; ++j) {
+            const uint64_t idx = base + lane + G * j;
+            const bool ok = idx < e;
+            kk[j] = ok ? __ldg(p.ci + idx) : 0u;
+            aa[j] = ok ? __ldg(p.val + idx) : T(0);
+          }
+#pragma unroll
+          for (int t = 0; t < kWin; t += kU) {
+            if (t < int(cnt)) {
+              V bv[kU][NV];
+#pragma unroll
+              for (int u = 0; u < kU; ++u) {
+                const int q = t + u;
+                const uint32_t k = __shfl_sync(gm, kk[q / G], q % G, G);
+                if (q < int(cnt)) {
+                  const V* brow = Bv + uint64_t(k) * ldbv + lane;
+#pragma unroll
+                  for (int v = 0; v < NV; ++v)
+                    if (colok[v]) bv[u][v] = __ldg(brow + G * v);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < kU; ++u) {
+                const int q = t + u;
+                const T a = __shfl_sync(gm, aa[q / G], q % G, G);
+                if (q < int(cnt)) {
+#pragma unroll
+                  for (int v = 0; v < NV; ++v)
+                    if (colok[v]) acc[v] = vfma(a, bv[u][v], acc[v]);
+                }
+              }
+            }
+          }
+        }
+        if (starts && ends) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+            if (colok[v]) Cv[uint64_t(r) * ldcv + lane + G * v] = acc[v];
+        } else {
+          V* dst = reinterpret_cast<V*>(starts ? p.tail_val : p.head_val) +
+                   uint64_t(c) * (p.wstride / VEC);
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+            if (colok[v]) dst[lane + G * v] = acc[v];
+          if (starts) trow = int32_t(r);
+        }
+      }
+      ++r;
+      rs = re;
+      re = re_next;
+      if (r >= p.rows) break;
+    }
+    if (lane == 0) p.tail_row[c] = trow;
+  }
+}
+
+// Rows cut by chunk boundaries: C[r] = tail(c) + head(c+1) + head(c+2) + ...
+template <typename T, int VEC, int G, int NV>
+__global__ void __launch_bounds__(kThreads) spmm_fixup(const SpmmArgs<T> p) {
+  using V = typename VecOf<T, VEC>::type;
+  const uint32_t lane = threadIdx.x % G;
+  const uint32_t worker = (blockIdx.x * kThreads + threadIdx.x) / G;
+  const uint32_t nworkers = gridDim.x * (kThreads / G);
+  const uint32_t ws = p.wstride / VEC;
+  V* __restrict__ Cv = reinterpret_cast<V*>(p.C);
+  const V* hv = reinterpret_cast<const V*>(p.head_val);
+  const V* tv = reinterpret_cast<const V*>(p.tail_val);
+  for (uint32_t c = worker; c < p.nchunks; c += nworkers) {
+    const int32_t r = p.tail_row[c];
+    if (r < 0) continue;
+    const uint64_t re = p.rp[r + 1];
+    V acc[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      if (lane + G * v < p.nvec) acc[v] = tv[uint64_t(c) * ws + lane + G * v];
+    for (uint32_t c2 = c + 1; c2 < p.nchunks; ++c2) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        if (lane + G * v < p.nvec)
+          acc[v] = vadd(acc[v], hv[uint64_t(c2) * ws + lane + G * v]);
+      if (re <= umin(uint64_t(c2 + 1) * p.Q, p.nnz)) break;
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      if (lane + G * v < p.nvec)
+        Cv[uint64_t(r) * (p.ldc / VEC) + lane + G * v] = acc[v];
+  }
+}
+
+struct Plan {
+  int G = 32, NV = 1, blocks = 0;
+  uint32_t nchunks = 0;
+  uint64_t Q = 0;
+};
+
+template <typename T, int VEC, int G, int NV>
+void launch(const SpmmArgs<T>& a, int blocks, int fix_blocks,
+            cudaStream_t s) {
+  spmm_chunks<T, VEC, G, NV><<<blocks, kThreads, 0, s>>>(a);
+  spmm_fixup<T, VEC, G, NV><<<fix_blocks, kThreads, 0, s>>>(a);
+}
+
+template <typename T, int VEC>
+void dispatch(const SpmmArgs<T>& a, int G, int NV, int blocks, int fix_blocks,
+              cudaStream_t s) {
+  switch (G) {
+    case 1: launch<T, VEC, 1, 1>(a, blocks, fix_blocks, s); break;
+    case 2: launch<T, VEC, 2, 1>(a, blocks, fix_blocks, s); break;
+    case 4: launch<T, VEC, 4, 1>(a, blocks, fix_blocks, s); break;
+    case 8: launch<T, VEC, 8, 1>(a, blocks, fix_blocks, s); break;
+    case 16: launch<T, VEC, 16, 1>(a, blocks, fix_blocks, s); break;
+    default:
+      if (NV == 1)
+        launch<T, VEC, 32, 1>(a, blocks, fix_blocks, s);
+      else if (NV == 2)
+        launch<T, VEC, 32, 2>(a, blocks, fix_blocks, s);
+      else
+        launch<T, VEC, 32, 4>(a, blocks, fix_blocks, s);
+  }
+}
+
+constexpr int kMaxNV = 4;
+
+// Panel width in vectors handled by one launch pair.
+inline uint32_t panel_vecs() { return 32u * kMaxNV; }
+
+inline uint32_t chunk_count(uint64_t nnz, uint32_t workers) {
+  // ~8 chunks per resident worker for tail smoothing, >= 64 nnz each.
+  uint64_t by_size = ceil_div(nnz, 64);
+  uint64_t by_workers = uint64_t(workers) * 8;
+  uint64_t n = std::max<uint64_t>(1, std::min(by_size, by_workers));
+  return uint32_t(std::min<uint64_t>(n, 1u << 30));
+}
+
+inline int groups_for(uint32_t nvec, int* NV) {
+  if (nvec >= 32) {
+    *NV = int(std::min<uint32_t>(kMaxNV, uint32_t(ceil_div(nvec, 32))));
+    if (*NV == 3) *NV = 4;
+    return 32;
+  }
+  *NV = 1;
+  int g = 1;
+  while (uint32_t(g) < nvec) g <<= 1;
+  return g;
+}
+
+struct SpmmPlan {
+  int VEC = 1, blocks = 0, fix_blocks = 0;
+  uint32_t pv = 0, nchunks = 0, wstride = 0;
+  uint64_t Q = 0;
+  size_t bytes = 0;
+};
+
+template <typename T>
+SpmmPlan make_plan(uint64_t nnz, uint32_t n, bool vec_ok) {
+  constexpr int VV = sizeof(T) == 4 ? 4 : 2;
+  SpmmPlan P;
+  P.VEC = vec_ok ? VV : 1;
+  const uint32_t nvec_total = n / P.VEC;
+  const int sms = num_sms();
+  P.pv = std::min<uint32_t>(nvec_total, panel_vecs());
+  int NV = 1;
+  const int G = groups_for(P.pv, &NV);
+  const int blocks_max = sms * 8;  // 8 x 256 threads per SM (register bound)
+  const uint32_t per_block = kThreads / G;
+  const uint32_t workers = uint32_t(blocks_max) * per_block;
+  const uint32_t nchunks = chunk_count(std::max<uint64_t>(nnz, 1), workers);
+  P.Q = ceil_div(std::max<uint64_t>(nnz, 1), nchunks);
+  P.nchunks = uint32_t(ceil_div(std::max<uint64_t>(nnz, 1), P.Q));
+  P.wstride = uint32_t(ceil_div(uint64_t(P.pv) * P.VEC, 4) * 4);
+  P.bytes = 2 * size_t(P.nchunks) * P.wstride * sizeof(T) +
+            size_t(P.nchunks) * 4 + 256;
+  P.blocks = int(std::min<uint64_t>(blocks_max, ceil_div(P.nchunks, per_block)));
+  P.fix_blocks = int(std::min<uint64_t>(sms * 4, ceil_div(P.nchunks, per_block)));
+  return P;
+}
+
+template <typename T>
+size_t workspace_bytes_impl(uint32_t rows, uint64_t nnz, uint32_t n) {
+  (void)rows;
+  return std::max(make_plan<T>(nnz, n, true).bytes,
+                  make_plan<T>(nnz, n, false).bytes);
+}
+
+template <typename T>
+int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
+              const uint32_t* rp, const uint32_t* ci, const T* val, const T* B,
+              uint64_t ldb, T* C, uint64_t ldc, void* ws, size_t ws_bytes,
+              rdmm_stream_t stream, uint64_t* flops) {
+  if (flops) *flops = 2ull * nnz * n;
+  if (ldb < n || ldc < n)
+    return fail(RDMM_ERR_DIMENSION, "spmm: leading dimension smaller than n");
+  if (rows == 0 || n == 0 || nnz == 0) return RDMM_OK;
+  if (!rp || !ci || !val || !B || !C)
+    return fail(RDMM_ERR_INVALID, "spmm: null device pointer");
+  (void)cols;
+  cudaStream_t s = as_stream(stream);
+  constexpr int VV = sizeof(T) == 4 ? 4 : 2;
+  const bool vec_ok = n % VV == 0 && ldb % VV == 0 && ldc % VV == 0 &&
+                      (reinterpret_cast<uintptr_t>(B) % 16) == 0 &&
+                      (reinterpret_cast<uintptr_t>(C) % 16) == 0;
+  const SpmmPlan P = make_plan<T>(nnz, n, vec_ok);
+  void* w = ws;
+  if (!w || ws_bytes < P.bytes) {
+    if (ws) return fail(RDMM_ERR_INVALID, "spmm: workspace too small");
+    w = scratch(P.bytes, 0);
+    if (!w) return fail(RDMM_ERR_CUDA, "spmm: scratch allocation failed");
+  }
+  SpmmArgs<T> a{};
+  a.rp = rp;
+  a.ci = ci;
+  a.val = val;
+  a.ldb = ldb;
+  a.ldc = ldc;
+  a.nnz = nnz;
+  a.Q = P.Q;
+  a.rows = rows;
+  a.nchunks = P.nchunks;
+  a.wstride = P.wstride;
+  char* base = static_cast<char*>(w);
+  const size_t vbytes = size_t(P.nchunks) * P.wstride * sizeof(T);
+  a.head_val = reinterpret_cast<T*>(base);
+  a.tail_val = reinterpret_cast<T*>(base + vbytes);
+  a.tail_row = reinterpret_cast<int32_t*>(base + 2 * vbytes);
+  const uint32_t nvec_total = n / P.VEC;
+  for (uint32_t v0 = 0; v0 < nvec_total; v0 += P.pv) {
+    const uint32_t nv = std::min<uint32_t>(P.pv, nvec_total - v0);
+    int nvp = 1;
+    const int g = groups_for(nv, &nvp);
+    a.B = B + uint64_t(v0) * P.VEC;
+    a.C = C + uint64_t(v0) * P.VEC;
+    a.nvec = nv;
+    if (P.VEC == 1)
+      dispatch<T, 1>(a, g, nvp, P.blocks, P.fix_blocks, s);
+    else
+      dispatch<T, VV>(a, g, nvp, P.blocks, P.fix_blocks, s);
+  }
+  RDMM_CUDA_TRY(cudaGetLastError());
+  return RDMM_OK;
+}
+
+}  // namespace
+}  // namespace rdmm_impl
+
+using namespace rdmm_impl;
+
+extern "C" size_t rdmm_spmm_workspace_bytes(uint32_t rows, uint64_t nnz,
+                                            uint32_t n, int dtype_bytes) {
+  return dtype_bytes == 8 ? workspace_bytes_impl<double>(rows, nnz, n)
+                          : workspace_bytes_impl<float>(rows, nnz, n);
+}
+
+extern "C" int rdmm_spmm_csr_f32(uint32_t rows, uint32_t cols, uint32_t n,
+                                 uint64_t nnz, const uint32_t* row_ptr,
+                                 const uint32_t* col_idx, const float* val,
+                                 const float* B, uint64_t ldb, float* C,
+                                 uint64_t ldc, void* workspace,
+                                 size_t workspace_bytes, rdmm_stream_t stream,
+                                 uint64_t* flops) {
+  return spmm_impl<float>(rows, cols, n, nnz, row_ptr, col_idx, val, B, ldb, C,
+                          ldc, workspace, workspace_bytes, stream, flops);
+}
+
+extern "C" int rdmm_spmm_csr_f64(uint32_t rows, uint32_t cols, uint32_t n,
+                                 uint64_t nnz, const uint32_t* row_ptr,
+                                 const uint32_t* col_idx, const double* val,
+                                 const double* B, uint64_t ldb, double* C,
+                                 uint64_t ldc, void* workspace,
+                                 size_t workspace_bytes, rdmm_stream_t stream,
+                                 uint64_t* flops) {
+  return spmm_impl<double>(rows, cols, n, nnz, row_ptr, col_idx, val, B, ldb,
+                           C, ldc, workspace, workspace_bytes, stream, flops);
+}

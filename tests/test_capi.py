@@ -1,0 +1,55 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads and exports
+every entry point include/*.h declares (no device calls)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared(header):
+    src = open(os.path.join(ROOT, "include", header)).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rdmm_[a-z0-9_]+)\s*\(", src)))
+
+
+def exported(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True,
+                         text=True, check=True).stdout
+    return {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+
+
+def test_cuda_capi_exports_every_declared_symbol():
+    import paper_2311_18141_b200._lib as L
+
+    names = declared("rdmm_cuda.h")
+    assert len(names) >= 10
+    syms = exported(L.LIB_PATH)
+    missing = [n for n in names if n not in syms]
+    assert not missing, missing
+    lib = ctypes.CDLL(L.LIB_PATH)
+    for n in names:
+        assert hasattr(lib, n)
+
+
+def test_error_taxonomy_mapping():
+    import paper_2311_18141_b200 as rd
+
+    assert issubclass(rd.HeapExhaustedError, rd.FabricError)
+    assert issubclass(rd.QueueFullError, rd.FabricError)
+    assert issubclass(rd.ProtocolError, rd.FabricError)
+    assert rd._lib.rdmm_version().startswith(b"rdmm-b200")
+
+
+def test_library_is_sm100a_only():
+    import paper_2311_18141_b200._lib as L
+
+    out = subprocess.run(["cuobjdump", "--list-elf", L.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    if not out:
+        pytest.skip("cuobjdump unavailable")
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
