@@ -79,6 +79,58 @@ int rdmm_spmm_csr_f64(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
                       double* C, uint64_t ldc, void* workspace,
                       size_t workspace_bytes, rdmm_stream_t stream,
                       uint64_t* flops);
+/* Extended form: dtype_bytes 4|8 and flags.
+ *   RDMM_SPMM_C_ZERO      C is all-zero on entry (a fresh tile): rows with
+ *                         nonzeros are written, C is never read; results are
+ *                         identical to the accumulate form on a zero C.
+ *   RDMM_SPMM_NO_PREFETCH disable the L2 prefetch of the next window's B rows.
+ */
+#define RDMM_SPMM_C_ZERO 1u
+#define RDMM_SPMM_NO_PREFETCH 2u
+int rdmm_spmm_csr_ex(int dtype_bytes, uint32_t rows, uint32_t cols, uint32_t n,
+                     uint64_t nnz, const uint32_t* row_ptr,
+                     const uint32_t* col_idx, const void* val, const void* B,
+                     uint64_t ldb, void* C, uint64_t ldc, unsigned flags,
+                     void* workspace, size_t workspace_bytes,
+                     rdmm_stream_t stream, uint64_t* flops);
+
+/* ---------------------------------------------------------------- SpGEMM */
+/*
+ * C = sum_t A_t * B_t  over a list of terms, rows x ncols, sorted rows,
+ * cancelled zeros kept (reference spgemm_local, tile.hpp:211-255).  A term
+ * whose a_row_ptr is NULL is an identity term contributing B_t as-is, so
+ *   spgemm_local(a,b)  = { a*b }                          (tile.hpp:211)
+ *   csr_add(a,b)       = { I*a, I*b }                     (tile.hpp:257)
+ *   stationary-C tile  = { I*C0, A(i,0)B(0,j), ... }      (algos.hpp:250-263)
+ * Two calls: rdmm_spgemm_symbolic bins rows, counts distinct columns, writes
+ * c_row_ptr (rows+1, device) and returns the output nnz and the reference
+ * FlopMeter flops (2 * multiply-adds, tile.hpp:197-209) on the host (it
+ * synchronises the stream); the caller allocates col_idx/values of c_nnz and
+ * calls rdmm_spgemm_numeric.  Column indices are bit-exact with the
+ * reference; values are summed in hardware order (exact for integer-valued
+ * data, within rounding otherwise).  All operand pointers are device
+ * pointers and must stay valid until rdmm_spgemm_numeric returns.
+ */
+typedef struct {
+  const uint32_t* a_row_ptr; /* NULL: identity term */
+  const uint32_t* a_col_idx;
+  const void* a_val;
+  const uint32_t* b_row_ptr;
+  const uint32_t* b_col_idx;
+  const void* b_val;
+} rdmm_spgemm_term;
+typedef struct rdmm_spgemm_plan rdmm_spgemm_plan;
+int rdmm_spgemm_symbolic(uint32_t rows, uint32_t ncols, int dtype_bytes,
+                         const rdmm_spgemm_term* terms, int nterms,
+                         uint32_t* c_row_ptr, rdmm_spgemm_plan** plan,
+                         uint64_t* c_nnz, uint64_t* flops,
+                         rdmm_stream_t stream);
+int rdmm_spgemm_numeric(rdmm_spgemm_plan* plan, uint32_t* c_col_idx,
+                        void* c_val, rdmm_stream_t stream);
+void rdmm_spgemm_plan_destroy(rdmm_spgemm_plan* plan);
+/* rows per symbolic / numeric tier (6 each: 5 hash tiers + dense) */
+int rdmm_spgemm_plan_info(const rdmm_spgemm_plan* plan, uint32_t* sym_tiers,
+                          uint32_t* num_tiers);
 
 /* --------------------------------------------------------- dense accumulate */
 /* c[i] += x[i] for i < count (reference dense_add_into, tile.hpp:300-307).

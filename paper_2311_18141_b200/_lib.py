@@ -79,6 +79,22 @@ rdmm_spmm_workspace_bytes = _fn("rdmm_spmm_workspace_bytes", [u32, u64, u32, cin
 _spmm_args = [u32, u32, u32, u64, vp, vp, vp, vp, u64, vp, u64, vp, sz, vp, P(u64)]
 rdmm_spmm_csr_f32 = _fn("rdmm_spmm_csr_f32", _spmm_args)
 rdmm_spmm_csr_f64 = _fn("rdmm_spmm_csr_f64", _spmm_args)
+rdmm_spmm_csr_ex = _fn("rdmm_spmm_csr_ex", [cint, u32, u32, u32, u64, vp, vp, vp, vp, u64, vp,
+                                            u64, C.c_uint, vp, sz, vp, P(u64)])
+SPMM_C_ZERO = 1
+SPMM_NO_PREFETCH = 2
+
+
+class SpgemmTerm(C.Structure):
+    _fields_ = [("a_row_ptr", vp), ("a_col_idx", vp), ("a_val", vp),
+                ("b_row_ptr", vp), ("b_col_idx", vp), ("b_val", vp)]
+
+
+rdmm_spgemm_symbolic = _fn("rdmm_spgemm_symbolic", [u32, u32, cint, P(SpgemmTerm), cint, vp,
+                                                    P(vp), P(u64), P(u64), vp])
+rdmm_spgemm_numeric = _fn("rdmm_spgemm_numeric", [vp, vp, vp, vp])
+rdmm_spgemm_plan_destroy = _fn("rdmm_spgemm_plan_destroy", [vp], None)
+rdmm_spgemm_plan_info = _fn("rdmm_spgemm_plan_info", [vp, P(u32), P(u32)])
 rdmm_dense_add_into_f32 = _fn("rdmm_dense_add_into_f32", [u32, u32, vp, u64, vp, u64, vp])
 rdmm_dense_add_into_f64 = _fn("rdmm_dense_add_into_f64", [u32, u32, vp, u64, vp, u64, vp])
 rdmm_gen_rng_at = _fn("rdmm_gen_rng_at", [u64, u64, u64, vp, vp])

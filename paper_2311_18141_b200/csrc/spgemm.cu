@@ -1,0 +1,688 @@
+// spgemm.cu -- C = sum_t A_t * B_t (+ identity terms) on sm_100a: the
+// row-wise Gustavson product of the reference, generalised to a list of
+// terms so that one kernel family covers
+//   spgemm_local(a, b)        tile.hpp:211-255   one term  A*B
+//   csr_add(a, b)             tile.hpp:257-288   two identity terms  I*a + I*b
+//   stationary-C accumulate   algos.hpp:250-263  I*C0 + sum_k A(i,k) B(k,j)
+//   queue drain accumulate    algos.hpp:278-293  I*C + sum_q I*P_q
+// Output rows are sorted and keep cancelled zeros (tile.hpp:211-213): the
+// pattern is the union of the symbolic products.
+//
+// Two passes:
+//  1. bin rows by the product count ub (= spgemm_flops/2 per row,
+//     tile.hpp:197-209); symbolic count of distinct columns per row in a
+//     shared-memory hash table sized to the bin (64 .. 32768 keys), or a
+//     global dense bitmap for the heaviest rows;  exclusive scan -> row_ptr.
+//  2. re-bin by the exact output count; numeric accumulation in a shared
+//     hash table (keys + values, load <= 0.5), bitonic sort in shared memory,
+//     store;  the heaviest rows use a per-CTA dense bitmap + dense value
+//     array whose in-order bitmap scan emits sorted columns directly.
+// Products of a row are enumerated "flattened": a window of G A-entries is
+// prefix-summed over their B-row lengths and the group's threads take
+// consecutive products, so B rows are read coalesced and hub rows of R-MAT
+// do not serialise on one thread.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace rdmm_impl {
+namespace {
+
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+constexpr int kTiers = 6;  // 5 hash tiers + dense
+
+template <typename T>
+struct TermDev {
+  const uint32_t* arp;  // nullptr: identity term (row r of B as-is)
+  const uint32_t* aci;
+  const T* av;
+  const uint32_t* brp;
+  const uint32_t* bci;
+  const T* bv;
+};
+
+// Symbolic tiers: ub <= limit -> table of 2*limit keys (64 .. 32768), G
+// threads per row (32 = a warp per row, 8 rows per CTA; else a CTA per row).
+__host__ __device__ constexpr uint32_t sym_limit(int i) {
+  return i == 0 ? 32u : i == 1 ? 256u : i == 2 ? 1024u : i == 3 ? 4096u : 16384u;
+}
+// Numeric tiers by exact output count (load factor <= 0.5).
+__host__ __device__ constexpr uint32_t num_limit(int i) {
+  return i == 0 ? 32u : i == 1 ? 256u : i == 2 ? 1024u : i == 3 ? 4096u : 8192u;
+}
+constexpr int kDenseThreads = 1024;
+
+__device__ __forceinline__ uint32_t hslot(uint32_t key, int log2t) {
+  return (key * 0x9E3779B1u) >> (32 - log2t);
+}
+
+template <int G>
+__device__ __forceinline__ void gsync() {
+  if constexpr (G == 32)
+    __syncwarp();
+  else
+    __syncthreads();
+}
+
+// Exclusive scan over the G threads of a group; returns the group total.
+template <int G>
+__device__ __forceinline__ uint32_t gscan(uint32_t v, uint32_t* sums,
+                                          uint32_t& total) {
+  const uint32_t tg = threadIdx.x % G, lane = tg & 31, warp = tg >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= uint32_t(off)) x += y;
+  }
+  if constexpr (G == 32) {
+    total = __shfl_sync(0xffffffffu, x, 31);
+    return x - v;
+  } else {
+    constexpr int W = G / 32;
+    if (lane == 31) sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t s = lane < uint32_t(W) ? sums[lane] : 0u;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, s, off);
+        if (lane >= uint32_t(off)) s += y;
+      }
+      if (lane < uint32_t(W)) sums[lane] = s;
+    }
+    __syncthreads();
+    const uint32_t base = warp ? sums[warp - 1] : 0u;
+    total = sums[W - 1];
+    __syncthreads();
+    return base + x - v;
+  }
+}
+
+template <int G>
+__device__ __forceinline__ uint32_t gsum(uint32_t v, uint32_t* sums) {
+  uint32_t total;
+  gscan<G>(v, sums, total);
+  return total;
+}
+
+// Window scratch for one group (G entries).
+template <typename T, int G>
+struct Win {
+  uint32_t pre[G];
+  uint32_t bs[G];
+  T a[G];
+  uint32_t sums[32];
+};
+
+// Enumerate every product (column key, value) of row r over all terms and
+// hand it to ins(key, value).  Identity terms contribute row r of B.
+template <typename T, int G, bool kValues, class Ins>
+__device__ __forceinline__ void enumerate_row(uint32_t r,
+                                              const TermDev<T>* terms,
+                                              int nterms, Win<T, G>& w,
+                                              Ins ins) {
+  const uint32_t tg = threadIdx.x % G;
+  for (int t = 0; t < nterms; ++t) {
+    const TermDev<T> tm = terms[t];
+    const bool ident = tm.arp == nullptr;
+    const uint32_t s0 = ident ? 0u : __ldg(tm.arp + r);
+    const uint32_t s1 = ident ? 1u : __ldg(tm.arp + r + 1);
+    for (uint32_t base = s0; base < s1; base += G) {
+      const uint32_t e = base + tg;
+      uint32_t len = 0, bs = 0;
+      T a = T(1);
+      if (e < s1) {
+        const uint32_t k = ident ? r : __ldg(tm.aci + e);
+        if (kValues && !ident) a = __ldg(tm.av + e);
+        bs = __ldg(tm.brp + k);
+        len = __ldg(tm.brp + k + 1) - bs;
+      }
+      uint32_t total;
+      const uint32_t ex = gscan<G>(len, w.sums, total);
+      w.pre[tg] = ex;
+      w.bs[tg] = bs;
+      if (kValues) w.a[tg] = a;
+      gsync<G>();
+      const uint32_t nvalid = min(uint32_t(G), s1 - base);
+      for (uint32_t p = tg; p < total; p += G) {
+        uint32_t lo = 0, hi = nvalid;
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (w.pre[mid] <= p)
+            lo = mid;
+          else
+            hi = mid;
+        }
+        const uint32_t tt = w.bs[lo] + (p - w.pre[lo]);
+        const uint32_t key = __ldg(tm.bci + tt);
+        T v = T(0);
+        if (kValues) v = ident ? __ldg(tm.bv + tt) : w.a[lo] * __ldg(tm.bv + tt);
+        ins(key, v);
+      }
+      gsync<G>();
+    }
+  }
+}
+
+// ------------------------------------------------------------ binning
+
+// Warp per row: ub[r] = number of products; bin by symbolic tier.
+template <typename T>
+__global__ void k_bin_sym(uint32_t rows, const TermDev<T>* terms, int nterms,
+                          uint32_t* lists, uint32_t* tier_count,
+                          unsigned long long* total_ub, uint64_t* cnt64) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = warp; r < rows; r += nwarps) {
+    unsigned long long ub = 0;
+    for (int t = 0; t < nterms; ++t) {
+      const TermDev<T> tm = terms[t];
+      if (tm.arp == nullptr) {
+        if (lane == 0) ub += __ldg(tm.brp + r + 1) - __ldg(tm.brp + r);
+        continue;
+      }
+      const uint32_t s0 = __ldg(tm.arp + r), s1 = __ldg(tm.arp + r + 1);
+      for (uint32_t e = s0 + lane; e < s1; e += 32) {
+        const uint32_t k = __ldg(tm.aci + e);
+        ub += __ldg(tm.brp + k + 1) - __ldg(tm.brp + k);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) ub += __shfl_xor_sync(0xffffffffu, ub, off);
+    if (lane == 0) {
+      cnt64[r] = 0;
+      if (ub) {
+        atomicAdd(total_ub, ub);
+        int tier = 5;
+        for (int i = 0; i < 5; ++i)
+          if (ub <= sym_limit(i)) {
+            tier = i;
+            break;
+          }
+        const uint32_t pos = atomicAdd(tier_count + tier, 1u);
+        lists[size_t(tier) * rows + pos] = r;
+      }
+    }
+  }
+}
+
+__global__ void k_bin_num(uint32_t rows, const uint64_t* cnt64, uint32_t* lists,
+                          uint32_t* tier_count) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += gridDim.x * blockDim.x) {
+    const uint64_t c = cnt64[r];
+    if (!c) continue;
+    int tier = 5;
+    for (int i = 0; i < 5; ++i)
+      if (c <= num_limit(i)) {
+        tier = i;
+        break;
+      }
+    const uint32_t pos = atomicAdd(tier_count + tier, 1u);
+    lists[size_t(tier) * rows + pos] = r;
+  }
+}
+
+// ------------------------------------------------------------ hash tiers
+
+template <typename T, int TAB, int G>
+__global__ void __launch_bounds__(G == 32 ? 256 : G)
+    k_sym_hash(const uint32_t* __restrict__ list, uint32_t count,
+               const TermDev<T>* terms, int nterms, uint64_t* cnt64) {
+  constexpr int RPB = G == 32 ? 8 : 1;  // rows per block
+  constexpr int LOG2T = __builtin_ctz(TAB);
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t grp = threadIdx.x / G, tg = threadIdx.x % G;
+  uint32_t* keys = reinterpret_cast<uint32_t*>(smem) + size_t(grp) * TAB;
+  Win<T, G>* win = reinterpret_cast<Win<T, G>*>(
+      smem + size_t(RPB) * TAB * 4) + grp;
+  for (uint32_t li = blockIdx.x * RPB + grp; li - grp < count;
+       li += gridDim.x * RPB) {
+    const bool active = li < count;  // whole group uniform
+    if (!active) {
+      if constexpr (G == 32) break;
+    }
+    const uint32_t r = active ? list[li] : 0u;
+    for (uint32_t i = tg; i < TAB; i += G) keys[i] = kEmpty;
+    gsync<G>();
+    if (active)
+      enumerate_row<T, G, false>(r, terms, nterms, *win, [&](uint32_t key, T) {
+        uint32_t s = hslot(key, LOG2T);
+        for (;;) {
+          const uint32_t old = atomicCAS(keys + s, kEmpty, key);
+          if (old == kEmpty || old == key) break;
+          s = (s + 1) & (TAB - 1);
+        }
+      });
+    gsync<G>();
+    uint32_t c = 0;
+    for (uint32_t i = tg; i < TAB; i += G) c += keys[i] != kEmpty;
+    c = gsum<G>(c, win->sums);
+    if (active && tg == 0) cnt64[r] = c;
+    gsync<G>();
+  }
+}
+
+template <typename T, int TAB, int G>
+__global__ void __launch_bounds__(G == 32 ? 256 : G)
+    k_num_hash(const uint32_t* __restrict__ list, uint32_t count,
+               const TermDev<T>* terms, int nterms,
+               const uint32_t* __restrict__ crp, uint32_t* __restrict__ cci,
+               T* __restrict__ cv, T ident_val) {
+  constexpr int RPB = G == 32 ? 8 : 1;
+  constexpr int LOG2T = __builtin_ctz(TAB);
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t grp = threadIdx.x / G, tg = threadIdx.x % G;
+  T* vals = reinterpret_cast<T*>(smem) + size_t(grp) * TAB;
+  uint32_t* keys =
+      reinterpret_cast<uint32_t*>(smem + size_t(RPB) * TAB * sizeof(T)) +
+      size_t(grp) * TAB;
+  Win<T, G>* win = reinterpret_cast<Win<T, G>*>(
+      smem + size_t(RPB) * TAB * (sizeof(T) + 4)) + grp;
+  for (uint32_t li = blockIdx.x * RPB + grp; li - grp < count;
+       li += gridDim.x * RPB) {
+    const bool active = li < count;
+    if (!active) {
+      if constexpr (G == 32) break;
+    }
+    const uint32_t r = active ? list[li] : 0u;
+    for (uint32_t i = tg; i < TAB; i += G) {
+      keys[i] = kEmpty;
+      vals[i] = ident_val;
+    }
+    gsync<G>();
+    if (active)
+      enumerate_row<T, G, true>(r, terms, nterms, *win, [&](uint32_t key, T v) {
+        uint32_t s = hslot(key, LOG2T);
+        for (;;) {
+          const uint32_t old = atomicCAS(keys + s, kEmpty, key);
+          if (old == kEmpty || old == key) break;
+          s = (s + 1) & (TAB - 1);
+        }
+        atomicAdd(vals + s, v);
+      });
+    gsync<G>();
+    // bitonic sort (keys, vals) ascending; empty keys sort last
+    for (uint32_t k = 2; k <= uint32_t(TAB); k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = tg; i < uint32_t(TAB); i += G) {
+          const uint32_t ixj = i ^ j;
+          if (ixj > i) {
+            const uint32_t ki = keys[i], kj = keys[ixj];
+            const bool up = (i & k) == 0;
+            if ((ki > kj) == up) {
+              keys[i] = kj;
+              keys[ixj] = ki;
+              const T t = vals[i];
+              vals[i] = vals[ixj];
+              vals[ixj] = t;
+            }
+          }
+        }
+        gsync<G>();
+      }
+    }
+    if (active) {
+      const uint32_t o = crp[r], n = crp[r + 1] - o;
+      for (uint32_t i = tg; i < n; i += G) {
+        cci[o + i] = keys[i];
+        cv[o + i] = vals[i];
+      }
+    }
+    gsync<G>();
+  }
+}
+
+// ------------------------------------------------------------ dense tier
+
+template <typename T>
+__global__ void __launch_bounds__(kDenseThreads)
+    k_sym_dense(const uint32_t* __restrict__ list, uint32_t count,
+                const TermDev<T>* terms, int nterms, uint64_t* cnt64,
+                uint32_t* bitmaps, uint32_t nwords) {
+  constexpr int G = kDenseThreads;
+  __shared__ Win<T, G> win;
+  uint32_t* bm = bitmaps + size_t(blockIdx.x) * nwords;
+  for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
+    const uint32_t r = list[li];
+    enumerate_row<T, G, false>(r, terms, nterms, win, [&](uint32_t key, T) {
+      const uint32_t bit = 1u << (key & 31);
+      if (!(bm[key >> 5] & bit)) atomicOr(bm + (key >> 5), bit);
+    });
+    __syncthreads();
+    uint32_t c = 0;
+    for (uint32_t i = threadIdx.x; i < nwords; i += G) {
+      c += __popc(bm[i]);
+      bm[i] = 0;
+    }
+    c = gsum<G>(c, win.sums);
+    if (threadIdx.x == 0) cnt64[r] = c;
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kDenseThreads)
+    k_num_dense(const uint32_t* __restrict__ list, uint32_t count,
+                const TermDev<T>* terms, int nterms,
+                const uint32_t* __restrict__ crp, uint32_t* __restrict__ cci,
+                T* __restrict__ cv, uint32_t* bitmaps, T* dense,
+                uint32_t nwords, uint32_t ncols, T ident_val) {
+  constexpr int G = kDenseThreads;
+  __shared__ Win<T, G> win;
+  uint32_t* bm = bitmaps + size_t(blockIdx.x) * nwords;
+  T* dv = dense + size_t(blockIdx.x) * ncols;
+  const uint32_t per = (nwords + G - 1) / G;
+  for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
+    const uint32_t r = list[li];
+    enumerate_row<T, G, true>(r, terms, nterms, win, [&](uint32_t key, T v) {
+      const uint32_t bit = 1u << (key & 31);
+      if (!(bm[key >> 5] & bit)) atomicOr(bm + (key >> 5), bit);
+      atomicAdd(dv + key, v);
+    });
+    __syncthreads();
+    const uint32_t w0 = threadIdx.x * per, w1 = min(w0 + per, nwords);
+    uint32_t c = 0;
+    for (uint32_t w = w0; w < w1; ++w) c += __popc(bm[w]);
+    uint32_t total;
+    uint32_t pos = crp[r] + gscan<G>(c, win.sums, total);
+    for (uint32_t w = w0; w < w1; ++w) {
+      uint32_t bits = bm[w];
+      bm[w] = 0;
+      while (bits) {
+        const uint32_t b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const uint32_t col = w * 32 + b;
+        cci[pos] = col;
+        cv[pos] = dv[col];
+        dv[col] = ident_val;
+        ++pos;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void k_fill(T* p, size_t n, T v) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_rowptr32(const uint64_t* pre, uint32_t n1, uint32_t* rp) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n1;
+       i += gridDim.x * blockDim.x)
+    rp[i] = uint32_t(pre[i]);
+}
+
+struct Buf {
+  void* p = nullptr;
+  size_t n = 0;
+  ~Buf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t ensure(size_t bytes) {
+    if (n >= bytes && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, bytes ? bytes : 8);
+    if (e == cudaSuccess) n = bytes;
+    return e;
+  }
+  template <typename X>
+  X* as() const {
+    return static_cast<X*>(p);
+  }
+};
+
+template <typename T, int TAB, int G>
+size_t hash_smem(bool numeric) {
+  constexpr int RPB = G == 32 ? 8 : 1;
+  return size_t(RPB) * TAB * (numeric ? sizeof(T) + 4 : 4) +
+         size_t(RPB) * sizeof(Win<T, G>);
+}
+
+template <typename T, int TAB, int G>
+int launch_sym_hash(const uint32_t* list, uint32_t count,
+                    const TermDev<T>* terms, int nterms, uint64_t* cnt64,
+                    cudaStream_t s) {
+  if (!count) return 0;
+  constexpr int RPB = G == 32 ? 8 : 1;
+  const size_t sm = hash_smem<T, TAB, G>(false);
+  auto fn = k_sym_hash<T, TAB, G>;
+  if (sm > 48 * 1024)
+    RDMM_CUDA_TRY(cudaFuncSetAttribute(
+        fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+  const int threads = G == 32 ? 256 : G;
+  const uint64_t blocks = std::min<uint64_t>(ceil_div(count, RPB),
+                                             uint64_t(num_sms()) * 64);
+  fn<<<unsigned(blocks), threads, sm, s>>>(list, count, terms, nterms, cnt64);
+  return 0;
+}
+
+template <typename T, int TAB, int G>
+int launch_num_hash(const uint32_t* list, uint32_t count,
+                    const TermDev<T>* terms, int nterms, const uint32_t* crp,
+                    uint32_t* cci, T* cv, T ident, cudaStream_t s) {
+  if (!count) return 0;
+  constexpr int RPB = G == 32 ? 8 : 1;
+  const size_t sm = hash_smem<T, TAB, G>(true);
+  auto fn = k_num_hash<T, TAB, G>;
+  if (sm > 48 * 1024)
+    RDMM_CUDA_TRY(cudaFuncSetAttribute(
+        fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+  const int threads = G == 32 ? 256 : G;
+  const uint64_t blocks = std::min<uint64_t>(ceil_div(count, RPB),
+                                             uint64_t(num_sms()) * 64);
+  fn<<<unsigned(blocks), threads, sm, s>>>(list, count, terms, nterms, crp,
+                                           cci, cv, ident);
+  return 0;
+}
+
+}  // namespace
+}  // namespace rdmm_impl
+
+using namespace rdmm_impl;
+
+struct rdmm_spgemm_plan {
+  int dtype = 4;
+  uint32_t rows = 0, ncols = 0;
+  int nterms = 0;
+  bool ident_only = false;
+  Buf terms, cnt64, pre64, lists, tcount, ub, scan_tmp, bitmaps, dense;
+  uint32_t sym_count[kTiers] = {0}, num_count[kTiers] = {0};
+  uint64_t nnz = 0, flops = 0;
+  uint32_t* c_row_ptr = nullptr;
+};
+
+namespace {
+
+template <typename T>
+int symbolic_impl(uint32_t rows, uint32_t ncols, const rdmm_spgemm_term* terms,
+                  int nterms, uint32_t* c_row_ptr, rdmm_spgemm_plan** out,
+                  uint64_t* c_nnz, uint64_t* flops, cudaStream_t s) {
+  auto* P = new rdmm_spgemm_plan();
+  std::unique_ptr<rdmm_spgemm_plan> guard(P);
+  P->dtype = sizeof(T);
+  P->rows = rows;
+  P->ncols = ncols;
+  P->nterms = nterms;
+  P->c_row_ptr = c_row_ptr;
+  std::vector<TermDev<T>> th(nterms > 0 ? nterms : 1);
+  bool ident_only = true;
+  for (int t = 0; t < nterms; ++t) {
+    th[t].arp = terms[t].a_row_ptr;
+    th[t].aci = terms[t].a_col_idx;
+    th[t].av = static_cast<const T*>(terms[t].a_val);
+    th[t].brp = terms[t].b_row_ptr;
+    th[t].bci = terms[t].b_col_idx;
+    th[t].bv = static_cast<const T*>(terms[t].b_val);
+    if (th[t].arp) ident_only = false;
+    if (!th[t].brp)
+      return fail(RDMM_ERR_INVALID, "spgemm: term without a B operand");
+  }
+  P->ident_only = ident_only;
+  RDMM_CUDA_TRY(P->terms.ensure(sizeof(TermDev<T>) * th.size()));
+  RDMM_CUDA_TRY(cudaMemcpyAsync(P->terms.p, th.data(),
+                                sizeof(TermDev<T>) * th.size(),
+                                cudaMemcpyHostToDevice, s));
+  RDMM_CUDA_TRY(P->cnt64.ensure(sizeof(uint64_t) * (size_t(rows) + 1)));
+  RDMM_CUDA_TRY(P->pre64.ensure(sizeof(uint64_t) * (size_t(rows) + 1)));
+  RDMM_CUDA_TRY(P->lists.ensure(sizeof(uint32_t) * size_t(kTiers) * (rows ? rows : 1)));
+  RDMM_CUDA_TRY(P->tcount.ensure(sizeof(uint32_t) * 2 * kTiers + 16));
+  RDMM_CUDA_TRY(cudaMemsetAsync(P->tcount.p, 0, sizeof(uint32_t) * 2 * kTiers + 16, s));
+  RDMM_CUDA_TRY(cudaMemsetAsync(P->cnt64.p, 0, sizeof(uint64_t) * (size_t(rows) + 1), s));
+  uint32_t* tc = P->tcount.as<uint32_t>();
+  auto* tub = reinterpret_cast<unsigned long long*>(tc + 2 * kTiers);
+  const TermDev<T>* td = P->terms.as<TermDev<T>>();
+  uint64_t* cnt = P->cnt64.as<uint64_t>();
+  uint32_t* lists = P->lists.as<uint32_t>();
+  if (rows && nterms) {
+    const unsigned blocks = unsigned(std::min<uint64_t>(
+        ceil_div(rows, 8), uint64_t(num_sms()) * 16));
+    k_bin_sym<T><<<blocks, 256, 0, s>>>(rows, td, nterms, lists, tc, tub, cnt);
+    RDMM_CUDA_TRY(cudaGetLastError());
+  }
+  uint32_t hc[2 * kTiers + 4];
+  RDMM_CUDA_TRY(cudaMemcpyAsync(hc, tc, sizeof(hc), cudaMemcpyDeviceToHost, s));
+  RDMM_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int i = 0; i < kTiers; ++i) P->sym_count[i] = hc[i];
+  P->flops = 2 * *reinterpret_cast<unsigned long long*>(hc + 2 * kTiers);
+  auto L = [&](int tier) { return lists + size_t(tier) * rows; };
+  int rc = 0;
+  rc |= launch_sym_hash<T, 64, 32>(L(0), hc[0], td, nterms, cnt, s);
+  rc |= launch_sym_hash<T, 512, 128>(L(1), hc[1], td, nterms, cnt, s);
+  rc |= launch_sym_hash<T, 2048, 256>(L(2), hc[2], td, nterms, cnt, s);
+  rc |= launch_sym_hash<T, 8192, 512>(L(3), hc[3], td, nterms, cnt, s);
+  rc |= launch_sym_hash<T, 32768, 1024>(L(4), hc[4], td, nterms, cnt, s);
+  if (rc) return rc;
+  const uint32_t nwords = uint32_t(ceil_div(ncols, 32));
+  if (hc[5]) {
+    const uint32_t blocks = std::min<uint32_t>(hc[5], uint32_t(num_sms()));
+    RDMM_CUDA_TRY(P->bitmaps.ensure(size_t(blocks) * nwords * 4));
+    RDMM_CUDA_TRY(cudaMemsetAsync(P->bitmaps.p, 0, size_t(blocks) * nwords * 4, s));
+    k_sym_dense<T><<<blocks, kDenseThreads, 0, s>>>(
+        L(5), hc[5], td, nterms, cnt, P->bitmaps.as<uint32_t>(), nwords);
+  }
+  RDMM_CUDA_TRY(cudaGetLastError());
+  // row_ptr = exclusive scan of the counts (64-bit, checked against uint32)
+  size_t tb = 0;
+  RDMM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, P->pre64.as<uint64_t>(),
+                                              int64_t(rows) + 1, s));
+  RDMM_CUDA_TRY(P->scan_tmp.ensure(tb));
+  RDMM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(P->scan_tmp.p, tb, cnt,
+                                              P->pre64.as<uint64_t>(),
+                                              int64_t(rows) + 1, s));
+  uint64_t total = 0;
+  RDMM_CUDA_TRY(cudaMemcpyAsync(&total, P->pre64.as<uint64_t>() + rows, 8,
+                                cudaMemcpyDeviceToHost, s));
+  if (rows) {
+    const unsigned nb = unsigned(std::min<uint64_t>(ceil_div(rows + 1, 256),
+                                                    uint64_t(num_sms()) * 8));
+    k_bin_num<<<nb, 256, 0, s>>>(rows, cnt, lists, tc + kTiers);
+  }
+  if (c_row_ptr) {
+    const unsigned nb = unsigned(std::min<uint64_t>(ceil_div(rows + 1, 256),
+                                                    uint64_t(num_sms()) * 8));
+    k_rowptr32<<<nb, 256, 0, s>>>(P->pre64.as<uint64_t>(), rows + 1, c_row_ptr);
+  }
+  RDMM_CUDA_TRY(cudaMemcpyAsync(hc, tc, sizeof(uint32_t) * 2 * kTiers,
+                                cudaMemcpyDeviceToHost, s));
+  RDMM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (total >= (1ull << 32))
+    return fail(RDMM_ERR_INVALID,
+                "spgemm: output nnz exceeds the uint32 index_t range");
+  for (int i = 0; i < kTiers; ++i) P->num_count[i] = hc[kTiers + i];
+  P->nnz = total;
+  if (c_nnz) *c_nnz = total;
+  if (flops) *flops = P->flops;
+  *out = guard.release();
+  return RDMM_OK;
+}
+
+template <typename T>
+int numeric_impl(rdmm_spgemm_plan* P, uint32_t* cci, T* cv, cudaStream_t s) {
+  if (P->nnz == 0) return RDMM_OK;
+  if (!P->c_row_ptr)
+    return fail(RDMM_ERR_INVALID, "spgemm numeric: plan has no row_ptr");
+  const TermDev<T>* td = P->terms.as<TermDev<T>>();
+  const int nt = P->nterms;
+  uint32_t* lists = P->lists.as<uint32_t>();
+  const uint32_t rows = P->rows;
+  auto L = [&](int tier) { return lists + size_t(tier) * rows; };
+  // -0.0 is the exact additive identity (keeps signed zeros of csr_add);
+  // products start from +0.0 like the reference accumulator (tile.hpp:232).
+  const T ident = P->ident_only ? T(-0.0) : T(0);
+  const uint32_t* crp = P->c_row_ptr;
+  const uint32_t* c = P->num_count;
+  int rc = 0;
+  rc |= launch_num_hash<T, 64, 32>(L(0), c[0], td, nt, crp, cci, cv, ident, s);
+  rc |= launch_num_hash<T, 512, 128>(L(1), c[1], td, nt, crp, cci, cv, ident, s);
+  rc |= launch_num_hash<T, 2048, 256>(L(2), c[2], td, nt, crp, cci, cv, ident, s);
+  rc |= launch_num_hash<T, 8192, 512>(L(3), c[3], td, nt, crp, cci, cv, ident, s);
+  rc |= launch_num_hash<T, 16384, 1024>(L(4), c[4], td, nt, crp, cci, cv, ident, s);
+  if (rc) return rc;
+  if (c[5]) {
+    const uint32_t nwords = uint32_t(ceil_div(P->ncols, 32));
+    const uint32_t blocks = std::min<uint32_t>(c[5], uint32_t(num_sms()));
+    RDMM_CUDA_TRY(P->bitmaps.ensure(size_t(blocks) * nwords * 4));
+    RDMM_CUDA_TRY(cudaMemsetAsync(P->bitmaps.p, 0, size_t(blocks) * nwords * 4, s));
+    RDMM_CUDA_TRY(P->dense.ensure(size_t(blocks) * P->ncols * sizeof(T)));
+    const size_t nd = size_t(blocks) * P->ncols;
+    k_fill<T><<<unsigned(std::min<uint64_t>(ceil_div(nd, 256), 4096)), 256, 0, s>>>(
+        P->dense.as<T>(), nd, ident);
+    k_num_dense<T><<<blocks, kDenseThreads, 0, s>>>(
+        L(5), c[5], td, nt, crp, cci, cv, P->bitmaps.as<uint32_t>(),
+        P->dense.as<T>(), nwords, P->ncols, ident);
+  }
+  RDMM_CUDA_TRY(cudaGetLastError());
+  return RDMM_OK;
+}
+
+}  // namespace
+
+extern "C" int rdmm_spgemm_symbolic(uint32_t rows, uint32_t ncols,
+                                    int dtype_bytes,
+                                    const rdmm_spgemm_term* terms, int nterms,
+                                    uint32_t* c_row_ptr,
+                                    rdmm_spgemm_plan** plan, uint64_t* c_nnz,
+                                    uint64_t* flops, rdmm_stream_t stream) {
+  if (!plan) return fail(RDMM_ERR_INVALID, "spgemm: null plan pointer");
+  *plan = nullptr;
+  if (nterms < 0 || (nterms > 0 && !terms))
+    return fail(RDMM_ERR_INVALID, "spgemm: bad term list");
+  return dtype_bytes == 8
+             ? symbolic_impl<double>(rows, ncols, terms, nterms, c_row_ptr,
+                                     plan, c_nnz, flops, as_stream(stream))
+             : symbolic_impl<float>(rows, ncols, terms, nterms, c_row_ptr,
+                                    plan, c_nnz, flops, as_stream(stream));
+}
+
+extern "C" int rdmm_spgemm_numeric(rdmm_spgemm_plan* plan, uint32_t* c_col_idx,
+                                   void* c_val, rdmm_stream_t stream) {
+  if (!plan) return fail(RDMM_ERR_INVALID, "spgemm: null plan");
+  return plan->dtype == 8
+             ? numeric_impl<double>(plan, c_col_idx, static_cast<double*>(c_val),
+                                    as_stream(stream))
+             : numeric_impl<float>(plan, c_col_idx, static_cast<float*>(c_val),
+                                   as_stream(stream));
+}
+
+extern "C" void rdmm_spgemm_plan_destroy(rdmm_spgemm_plan* plan) { delete plan; }
+
+extern "C" int rdmm_spgemm_plan_info(const rdmm_spgemm_plan* plan,
+                                     uint32_t* sym_tiers, uint32_t* num_tiers) {
+  if (!plan) return fail(RDMM_ERR_INVALID, "spgemm: null plan");
+  for (int i = 0; i < kTiers; ++i) {
+    if (sym_tiers) sym_tiers[i] = plan->sym_count[i];
+    if (num_tiers) num_tiers[i] = plan->num_count[i];
+  }
+  return RDMM_OK;
+}

@@ -19,6 +19,8 @@
 //    broadcast with shuffles.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace rdmm_impl {
@@ -90,6 +92,7 @@ struct SpmmArgs {
   uint64_t ldb, ldc;
   uint64_t nnz, Q;
   uint32_t rows, nvec, nchunks, wstride;
+  int prefetch;
 };
 
 template <int G>
@@ -106,9 +109,52 @@ constexpr int kThreads = 256;
 constexpr int kWin = 32;  // nonzeros staged per window
 constexpr int kU = 8;     // B-row gathers in flight per worker
 
-template <typename T, int VEC, int G, int NV>
-__global__ void __launch_bounds__(kThreads)
-    spmm_chunks(const SpmmArgs<T> p) {
+// Index of the first of the 32 window rows [rb, rb+32) whose end exceeds pos
+// (the row holding nonzero `pos`); 32 if every window row ends <= pos.
+template <int G, int SL>
+__device__ __forceinline__ uint32_t rows_done(const uint32_t (&rew)[SL],
+                                              uint64_t pos, unsigned gm) {
+  uint32_t n = 0;
+#pragma unroll
+  for (int j = 0; j < SL; ++j)
+    n += __popc(__ballot_sync(gm, uint64_t(rew[j]) <= pos) & gm);
+  return n;
+}
+
+template <int G, int SL>
+__device__ __forceinline__ uint32_t win_get(const uint32_t (&rew)[SL],
+                                            uint32_t idx, unsigned gm) {
+  uint32_t v = 0;
+#pragma unroll
+  for (int j = 0; j < SL; ++j) {
+    const uint32_t x = __shfl_sync(gm, rew[j], idx % G, G);
+    if (idx / G == uint32_t(j)) v = x;
+  }
+  return v;
+}
+
+template <int G, int SL>
+__device__ __forceinline__ void win_load(uint32_t (&rew)[SL],
+                                         const uint32_t* __restrict__ rp,
+                                         uint32_t rb, uint32_t rows,
+                                         uint32_t lane) {
+#pragma unroll
+  for (int j = 0; j < SL; ++j) {
+    const uint32_t rr = rb + lane + G * j;  // row whose end we hold
+    rew[j] = rr < rows ? __ldg(rp + rr + 1) : 0xFFFFFFFFu;
+  }
+}
+
+// Stream one nnz chunk [lo, hi): the chunk's nonzeros are consumed 32 at a
+// time regardless of row boundaries (col/val of the next window and an L2
+// prefetch of its B rows overlap the current window's gathers), rows are
+// tracked through a 32-entry window of row ends held in registers, and a row
+// is flushed to C (or to a carry slot if the chunk cuts it) when the stream
+// crosses its end.  CZERO: C is known to be zero on entry (first product
+// into a fresh tile), so C is written but never read.
+template <typename T, int VEC, int G, int NV, bool CZERO, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    spmm_stream(const SpmmArgs<T> p) {
   using V = typename VecOf<T, VEC>::type;
   constexpr int SL = kWin / G;  // staged entries per lane
   const unsigned gm = group_mask<G>();
@@ -118,6 +164,7 @@ __global__ void __launch_bounds__(kThreads)
   const V* __restrict__ Bv = reinterpret_cast<const V*>(p.B);
   V* __restrict__ Cv = reinterpret_cast<V*>(p.C);
   const uint64_t ldbv = p.ldb / VEC, ldcv = p.ldc / VEC;
+  const uint32_t row_bytes = p.nvec * VEC * sizeof(T);
   bool colok[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) colok[v] = lane + G * v < p.nvec;
@@ -128,82 +175,138 @@ __global__ void __launch_bounds__(kThreads)
     // row containing nonzero `lo`: largest r with rp[r] <= lo
     uint32_t l = 0, h = p.rows;
     while (h - l > 1) {
-      uint32_t m = (l + h) >> 1;
+      const uint32_t m = (l + h) >> 1;
       if (__ldg(p.rp + m) <= lo)
         l = m;
       else
         h = m;
     }
-    uint32_t r = l;
-    uint32_t rs = __ldg(p.rp + r);
-    uint32_t re = __ldg(p.rp + r + 1);
-    int32_t trow = -1;
-    while (rs < hi) {
-      const uint32_t re_next = (r + 2 <= p.rows) ? __ldg(p.rp + r + 2) : re;
-      const uint64_t s = umax(rs, lo), e = umin(re, hi);
-      if (s < e) {
-        const bool starts = rs >= lo, ends = re <= hi;
-        V acc[NV];
+    uint32_t rb = l, row = l;
+    uint32_t rew[SL];
+    win_load<G, SL>(rew, p.rp, rb, p.rows, lane);
+    bool starts = __ldg(p.rp + row) >= lo;
+    uint32_t rend = win_get<G, SL>(rew, 0, gm);
+    V acc[NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v)
-          acc[v] = (starts && colok[v]) ? Cv[uint64_t(r) * ldcv + lane + G * v]
-                                        : vzero<V>();
-        for (uint64_t base = s; base < e; base += kWin) {
-          const uint32_t cnt = uint32_t(umin(kWin, e - base));
-          uint32_t kk[SL];
-          T aa[SL];
+    for (int v = 0; v < NV; ++v)
+      acc[v] = (!CZERO && starts && colok[v])
+                   ? __ldcs(Cv + uint64_t(row) * ldcv + lane + G * v)
+                   : vzero<V>();
+    // first window of col/val
+    uint32_t kk[SL];
+    T aa[SL];
 #pragma unroll
-          for (int j = 0; j < SL; ++j) {
-            const uint64_t idx = base + lane + G * j;
-            const bool ok = idx < e;
-            kk[j] = ok ? __ldg(p.ci + idx) : 0u;
-            aa[j] = ok ? __ldg(p.val + idx) : T(0);
+    for (int j = 0; j < SL; ++j) {
+      const uint64_t idx = lo + lane + G * j;
+      const bool ok = idx < hi;
+      kk[j] = ok ? __ldcs(p.ci + idx) : 0u;
+      aa[j] = ok ? __ldcs(p.val + idx) : T(0);
+    }
+    for (uint64_t w = lo; w < hi; w += kWin) {
+      const uint32_t cnt = uint32_t(umin(kWin, hi - w));
+      // next window's col/val (software pipelined one window ahead)
+      uint32_t kn[SL];
+      T an[SL];
+#pragma unroll
+      for (int j = 0; j < SL; ++j) {
+        const uint64_t idx = w + kWin + lane + G * j;
+        const bool ok = idx < hi;
+        kn[j] = ok ? __ldcs(p.ci + idx) : 0u;
+        an[j] = ok ? __ldcs(p.val + idx) : T(0);
+      }
+#pragma unroll
+      for (int t = 0; t < kWin; t += kU) {
+        if (t < int(cnt)) {
+          V bv[kU][NV];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int q = t + u;
+            const uint32_t k = __shfl_sync(gm, kk[q / G], q % G, G);
+            if (q < int(cnt)) {
+              const V* brow = Bv + uint64_t(k) * ldbv + lane;
+#pragma unroll
+              for (int v = 0; v < NV; ++v)
+                if (colok[v]) bv[u][v] = __ldg(brow + G * v);
+            }
           }
+          if (t == kU && p.prefetch) {
+            // warm L2 with the next window's B rows (no registers held)
 #pragma unroll
-          for (int t = 0; t < kWin; t += kU) {
-            if (t < int(cnt)) {
-              V bv[kU][NV];
-#pragma unroll
-              for (int u = 0; u < kU; ++u) {
-                const int q = t + u;
-                const uint32_t k = __shfl_sync(gm, kk[q / G], q % G, G);
-                if (q < int(cnt)) {
-                  const V* brow = Bv + uint64_t(k) * ldbv + lane;
-#pragma unroll
-                  for (int v = 0; v < NV; ++v)
-                    if (colok[v]) bv[u][v] = __ldg(brow + G * v);
-                }
-              }
-#pragma unroll
-              for (int u = 0; u < kU; ++u) {
-                const int q = t + u;
-                const T a = __shfl_sync(gm, aa[q / G], q % G, G);
-                if (q < int(cnt)) {
-#pragma unroll
-                  for (int v = 0; v < NV; ++v)
-                    if (colok[v]) acc[v] = vfma(a, bv[u][v], acc[v]);
-                }
+            for (int j = 0; j < SL; ++j) {
+              if (w + kWin + lane + G * j < hi) {
+                const char* rowp = reinterpret_cast<const char*>(
+                    Bv + uint64_t(kn[j]) * ldbv);
+                for (uint32_t off = 0; off < row_bytes; off += 128)
+                  asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + off));
               }
             }
           }
-        }
-        if (starts && ends) {
 #pragma unroll
-          for (int v = 0; v < NV; ++v)
-            if (colok[v]) Cv[uint64_t(r) * ldcv + lane + G * v] = acc[v];
-        } else {
-          V* dst = reinterpret_cast<V*>(starts ? p.tail_val : p.head_val) +
-                   uint64_t(c) * (p.wstride / VEC);
+          for (int u = 0; u < kU; ++u) {
+            const int q = t + u;
+            const T a = __shfl_sync(gm, aa[q / G], q % G, G);
+            if (q < int(cnt)) {
+              const uint64_t pos = w + q;
+              if (pos >= rend) {
+                // the stream crossed the end of `row`: it lies inside the
+                // chunk, so flush to C (or to the head slot if the chunk
+                // started inside it)
+                if (starts) {
 #pragma unroll
-          for (int v = 0; v < NV; ++v)
-            if (colok[v]) dst[lane + G * v] = acc[v];
-          if (starts) trow = int32_t(r);
+                  for (int v = 0; v < NV; ++v)
+                    if (colok[v])
+                      __stcs(Cv + uint64_t(row) * ldcv + lane + G * v, acc[v]);
+                } else {
+                  V* dst = reinterpret_cast<V*>(p.head_val) +
+                           uint64_t(c) * (p.wstride / VEC);
+#pragma unroll
+                  for (int v = 0; v < NV; ++v)
+                    if (colok[v]) dst[lane + G * v] = acc[v];
+                }
+                // next row holding `pos` (skips empty rows)
+                for (;;) {
+                  const uint32_t d = rows_done<G, SL>(rew, pos, gm);
+                  if (d < uint32_t(kWin)) {
+                    row = rb + d;
+                    rend = win_get<G, SL>(rew, d, gm);
+                    break;
+                  }
+                  rb += kWin;
+                  win_load<G, SL>(rew, p.rp, rb, p.rows, lane);
+                }
+                starts = true;
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+                  acc[v] = (!CZERO && colok[v])
+                               ? __ldcs(Cv + uint64_t(row) * ldcv + lane + G * v)
+                               : vzero<V>();
+              }
+#pragma unroll
+              for (int v = 0; v < NV; ++v)
+                if (colok[v]) acc[v] = vfma(a, bv[u][v], acc[v]);
+            }
+          }
         }
       }
-      ++r;
-      rs = re;
-      re = re_next;
-      if (r >= p.rows) break;
+#pragma unroll
+      for (int j = 0; j < SL; ++j) {
+        kk[j] = kn[j];
+        aa[j] = an[j];
+      }
+    }
+    // the chunk's last row
+    int32_t trow = -1;
+    if (rend <= hi && starts) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        if (colok[v]) __stcs(Cv + uint64_t(row) * ldcv + lane + G * v, acc[v]);
+    } else {
+      V* dst = reinterpret_cast<V*>(starts ? p.tail_val : p.head_val) +
+               uint64_t(c) * (p.wstride / VEC);
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        if (colok[v]) dst[lane + G * v] = acc[v];
+      if (starts) trow = int32_t(row);
     }
     if (lane == 0) p.tail_row[c] = trow;
   }
@@ -248,29 +351,49 @@ struct Plan {
   uint64_t Q = 0;
 };
 
+// RDMM_SPMM_OCC=4 selects the 64-register (4 CTAs/SM) build of the main
+// kernel; default is the unconstrained build.
+inline int occ_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("RDMM_SPMM_OCC");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <typename T, int VEC, int G, int NV>
-void launch(const SpmmArgs<T>& a, int blocks, int fix_blocks,
+void launch(const SpmmArgs<T>& a, bool czero, int blocks, int fix_blocks,
             cudaStream_t s) {
-  spmm_chunks<T, VEC, G, NV><<<blocks, kThreads, 0, s>>>(a);
+  if (G == 32 && NV == 1 && occ_variant() == 4) {
+    if (czero)
+      spmm_stream<T, VEC, G, NV, true, 4><<<blocks, kThreads, 0, s>>>(a);
+    else
+      spmm_stream<T, VEC, G, NV, false, 4><<<blocks, kThreads, 0, s>>>(a);
+  } else {
+    if (czero)
+      spmm_stream<T, VEC, G, NV, true, 1><<<blocks, kThreads, 0, s>>>(a);
+    else
+      spmm_stream<T, VEC, G, NV, false, 1><<<blocks, kThreads, 0, s>>>(a);
+  }
   spmm_fixup<T, VEC, G, NV><<<fix_blocks, kThreads, 0, s>>>(a);
 }
 
 template <typename T, int VEC>
-void dispatch(const SpmmArgs<T>& a, int G, int NV, int blocks, int fix_blocks,
-              cudaStream_t s) {
+void dispatch(const SpmmArgs<T>& a, bool cz, int G, int NV, int blocks,
+              int fix_blocks, cudaStream_t s) {
   switch (G) {
-    case 1: launch<T, VEC, 1, 1>(a, blocks, fix_blocks, s); break;
-    case 2: launch<T, VEC, 2, 1>(a, blocks, fix_blocks, s); break;
-    case 4: launch<T, VEC, 4, 1>(a, blocks, fix_blocks, s); break;
-    case 8: launch<T, VEC, 8, 1>(a, blocks, fix_blocks, s); break;
-    case 16: launch<T, VEC, 16, 1>(a, blocks, fix_blocks, s); break;
+    case 1: launch<T, VEC, 1, 1>(a, cz, blocks, fix_blocks, s); break;
+    case 2: launch<T, VEC, 2, 1>(a, cz, blocks, fix_blocks, s); break;
+    case 4: launch<T, VEC, 4, 1>(a, cz, blocks, fix_blocks, s); break;
+    case 8: launch<T, VEC, 8, 1>(a, cz, blocks, fix_blocks, s); break;
+    case 16: launch<T, VEC, 16, 1>(a, cz, blocks, fix_blocks, s); break;
     default:
       if (NV == 1)
-        launch<T, VEC, 32, 1>(a, blocks, fix_blocks, s);
+        launch<T, VEC, 32, 1>(a, cz, blocks, fix_blocks, s);
       else if (NV == 2)
-        launch<T, VEC, 32, 2>(a, blocks, fix_blocks, s);
+        launch<T, VEC, 32, 2>(a, cz, blocks, fix_blocks, s);
       else
-        launch<T, VEC, 32, 4>(a, blocks, fix_blocks, s);
+        launch<T, VEC, 32, 4>(a, cz, blocks, fix_blocks, s);
   }
 }
 
@@ -337,12 +460,21 @@ size_t workspace_bytes_impl(uint32_t rows, uint64_t nnz, uint32_t n) {
                   make_plan<T>(nnz, n, false).bytes);
 }
 
+inline int prefetch_default() {
+  static const int v = [] {
+    const char* e = std::getenv("RDMM_SPMM_PREFETCH");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <typename T>
 int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
               const uint32_t* rp, const uint32_t* ci, const T* val, const T* B,
-              uint64_t ldb, T* C, uint64_t ldc, void* ws, size_t ws_bytes,
-              rdmm_stream_t stream, uint64_t* flops) {
+              uint64_t ldb, T* C, uint64_t ldc, unsigned flags, void* ws,
+              size_t ws_bytes, rdmm_stream_t stream, uint64_t* flops) {
   if (flops) *flops = 2ull * nnz * n;
+  const bool czero = (flags & RDMM_SPMM_C_ZERO) != 0;
   if (ldb < n || ldc < n)
     return fail(RDMM_ERR_DIMENSION, "spmm: leading dimension smaller than n");
   if (rows == 0 || n == 0 || nnz == 0) return RDMM_OK;
@@ -372,6 +504,7 @@ int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
   a.rows = rows;
   a.nchunks = P.nchunks;
   a.wstride = P.wstride;
+  a.prefetch = (flags & RDMM_SPMM_NO_PREFETCH) ? 0 : prefetch_default();
   char* base = static_cast<char*>(w);
   const size_t vbytes = size_t(P.nchunks) * P.wstride * sizeof(T);
   a.head_val = reinterpret_cast<T*>(base);
@@ -386,9 +519,9 @@ int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
     a.C = C + uint64_t(v0) * P.VEC;
     a.nvec = nv;
     if (P.VEC == 1)
-      dispatch<T, 1>(a, g, nvp, P.blocks, P.fix_blocks, s);
+      dispatch<T, 1>(a, czero, g, nvp, P.blocks, P.fix_blocks, s);
     else
-      dispatch<T, VV>(a, g, nvp, P.blocks, P.fix_blocks, s);
+      dispatch<T, VV>(a, czero, g, nvp, P.blocks, P.fix_blocks, s);
   }
   RDMM_CUDA_TRY(cudaGetLastError());
   return RDMM_OK;
@@ -413,7 +546,7 @@ extern "C" int rdmm_spmm_csr_f32(uint32_t rows, uint32_t cols, uint32_t n,
                                  size_t workspace_bytes, rdmm_stream_t stream,
                                  uint64_t* flops) {
   return spmm_impl<float>(rows, cols, n, nnz, row_ptr, col_idx, val, B, ldb, C,
-                          ldc, workspace, workspace_bytes, stream, flops);
+                          ldc, 0u, workspace, workspace_bytes, stream, flops);
 }
 
 extern "C" int rdmm_spmm_csr_f64(uint32_t rows, uint32_t cols, uint32_t n,
@@ -424,5 +557,26 @@ extern "C" int rdmm_spmm_csr_f64(uint32_t rows, uint32_t cols, uint32_t n,
                                  size_t workspace_bytes, rdmm_stream_t stream,
                                  uint64_t* flops) {
   return spmm_impl<double>(rows, cols, n, nnz, row_ptr, col_idx, val, B, ldb,
-                           C, ldc, workspace, workspace_bytes, stream, flops);
+                           C, ldc, 0u, workspace, workspace_bytes, stream, flops);
+}
+
+extern "C" int rdmm_spmm_csr_ex(int dtype_bytes, uint32_t rows, uint32_t cols,
+                                uint32_t n, uint64_t nnz,
+                                const uint32_t* row_ptr,
+                                const uint32_t* col_idx, const void* val,
+                                const void* B, uint64_t ldb, void* C,
+                                uint64_t ldc, unsigned flags, void* workspace,
+                                size_t workspace_bytes, rdmm_stream_t stream,
+                                uint64_t* flops) {
+  if (dtype_bytes == 8)
+    return spmm_impl<double>(rows, cols, n, nnz, row_ptr, col_idx,
+                             static_cast<const double*>(val),
+                             static_cast<const double*>(B), ldb,
+                             static_cast<double*>(C), ldc, flags, workspace,
+                             workspace_bytes, stream, flops);
+  return spmm_impl<float>(rows, cols, n, nnz, row_ptr, col_idx,
+                          static_cast<const float*>(val),
+                          static_cast<const float*>(B), ldb,
+                          static_cast<float*>(C), ldc, flags, workspace,
+                          workspace_bytes, stream, flops);
 }

@@ -94,9 +94,11 @@ class DeviceCsr:
 
 
 def spmm_local(a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, stream=None,
-               workspace: torch.Tensor | None = None) -> FlopMeter:
+               workspace: torch.Tensor | None = None, c_zero: bool = False,
+               prefetch: bool = True) -> FlopMeter:
     """c += a @ b on the device; tile.hpp:170-188.  Raises DimensionError on
-    mismatch exactly like the reference (tile.hpp:173-174)."""
+    mismatch exactly like the reference (tile.hpp:173-174).  c_zero=True
+    asserts c is all-zero on entry (it is then written, never read)."""
     if a.cols != b.shape[0] or c.shape[0] != a.rows or c.shape[1] != b.shape[1]:
         raise L.DimensionError("spmm_local: dimension mismatch")
     if b.dtype != a.dtype or c.dtype != a.dtype:
@@ -105,13 +107,64 @@ def spmm_local(a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, stream=None,
         raise L.InvalidArgument("spmm_local: B and C must be row-major")
     n = b.shape[1]
     fl = C.c_uint64(0)
-    fn = L.rdmm_spmm_csr_f64 if a.dtype == torch.float64 else L.rdmm_spmm_csr_f32
     ws = workspace.data_ptr() if workspace is not None else None
     wsb = workspace.numel() * workspace.element_size() if workspace is not None else 0
-    L.check(fn(a.rows, a.cols, n, a.nnz, a.row_ptr.data_ptr(), a.col_idx.data_ptr(),
-               a.values.data_ptr(), b.data_ptr(), b.stride(0), c.data_ptr(), c.stride(0),
-               ws, wsb, _stream(stream), C.byref(fl)), "spmm_local")
+    flags = (L.SPMM_C_ZERO if c_zero else 0) | (0 if prefetch else L.SPMM_NO_PREFETCH)
+    L.check(L.rdmm_spmm_csr_ex(_wcode(a.dtype), a.rows, a.cols, n, a.nnz, a.row_ptr.data_ptr(),
+                               a.col_idx.data_ptr(), a.values.data_ptr(), b.data_ptr(),
+                               b.stride(0), c.data_ptr(), c.stride(0), flags, ws, wsb,
+                               _stream(stream), C.byref(fl)), "spmm_local")
     return FlopMeter(fl.value, c.shape[0] * c.shape[1])
+
+
+def spgemm_terms(rows: int, ncols: int, terms, dtype=torch.float32, device="cuda",
+                 stream=None, info: dict | None = None):
+    """C = sum_t A_t @ B_t over (A_t | None, B_t) pairs (None = identity),
+    sorted rows, cancelled zeros kept.  Returns (DeviceCsr, FlopMeter)."""
+    arr = (L.SpgemmTerm * max(1, len(terms)))()
+    for i, (a, b) in enumerate(terms):
+        if a is not None:
+            arr[i].a_row_ptr = a.row_ptr.data_ptr()
+            arr[i].a_col_idx = a.col_idx.data_ptr() if a.nnz else None
+            arr[i].a_val = a.values.data_ptr() if a.nnz else None
+        arr[i].b_row_ptr = b.row_ptr.data_ptr()
+        arr[i].b_col_idx = b.col_idx.data_ptr() if b.nnz else None
+        arr[i].b_val = b.values.data_ptr() if b.nnz else None
+    rp = torch.zeros(rows + 1, dtype=torch.int32, device=device)
+    plan = C.c_void_p()
+    nnz, fl = C.c_uint64(0), C.c_uint64(0)
+    L.check(L.rdmm_spgemm_symbolic(rows, ncols, _wcode(dtype), arr, len(terms), rp.data_ptr(),
+                                   C.byref(plan), C.byref(nnz), C.byref(fl), _stream(stream)),
+            "spgemm symbolic")
+    try:
+        out = DeviceCsr.empty(rows, ncols, nnz.value, dtype=dtype, device=device)
+        out.row_ptr = rp
+        if nnz.value:
+            L.check(L.rdmm_spgemm_numeric(plan, out.col_idx.data_ptr(), out.values.data_ptr(),
+                                          _stream(stream)), "spgemm numeric")
+        if info is not None:
+            st, nt = (C.c_uint32 * 6)(), (C.c_uint32 * 6)()
+            L.rdmm_spgemm_plan_info(plan, st, nt)
+            info["sym_tiers"], info["num_tiers"] = list(st), list(nt)
+    finally:
+        L.rdmm_spgemm_plan_destroy(plan)
+    return out, FlopMeter(fl.value, nnz.value)
+
+
+def spgemm_local(a: DeviceCsr, b: DeviceCsr, stream=None, info=None):
+    """(a @ b, FlopMeter) -- tile.hpp:211-255; DimensionError like :216-217."""
+    if a.cols != b.rows:
+        raise L.DimensionError("spgemm_local: dimension mismatch")
+    return spgemm_terms(a.rows, b.cols, [(a, b)], dtype=a.dtype, device=a.device,
+                        stream=stream, info=info)
+
+
+def csr_add(a: DeviceCsr, b: DeviceCsr, stream=None) -> DeviceCsr:
+    """Merged CSR sum, duplicates summed, zeros kept -- tile.hpp:257-288."""
+    if a.rows != b.rows or a.cols != b.cols:
+        raise L.DimensionError("csr_add: dimension mismatch")
+    return spgemm_terms(a.rows, a.cols, [(None, a), (None, b)], dtype=a.dtype,
+                        device=a.device, stream=stream)[0]
 
 
 def dense_add_into(c: torch.Tensor, x: torch.Tensor, stream=None) -> None:
