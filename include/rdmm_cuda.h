@@ -172,6 +172,168 @@ int rdmm_gen_finish(rdmm_gen_state* st, int dtype_bytes, uint32_t* row_ptr,
                     uint32_t* col_idx, void* values);
 void rdmm_gen_abort(rdmm_gen_state* st);
 
+/* ================================================================ fabric */
+/*
+ * The one-sided fabric (reference fabric.hpp:26-575) on B200:
+ *  - one DEVICE heap per rank (cudaMalloc on the rank's GPU, first-fit,
+ *    8-byte aligned -- fabric.hpp:277-360); every rank's heap is mapped into
+ *    every other rank's device address space (peer access inside a process,
+ *    CUDA IPC across processes), so a GlobalPtr resolves to a device address
+ *    any rank can copy from or load from over NVLink;
+ *  - a node-shared CONTROL segment (POSIX shared memory, pinned and mapped
+ *    into every rank's device): fetch-add cells, remote queues, the barrier
+ *    and the abort flag live here, so a reservation is one host atomic and a
+ *    queue push one host atomic + store;
+ *  - ranks are threads of one process (run_ranks, fabric.hpp:556-575) or one
+ *    process per GPU (torchrun) sharing the control segment by name.
+ * Host threads call these with the rank they act for (`caller`); calls for
+ * one rank must come from one thread at a time (fabric.hpp:414-415).
+ */
+typedef struct rdmm_fabric rdmm_fabric;
+
+/* GlobalPtr (fabric.hpp:30-36).  offset bit 63 set = control-segment cell. */
+typedef struct {
+  uint32_t rank;
+  uint32_t pad_;
+  uint64_t offset;
+  uint64_t length;
+} rdmm_gptr;
+#define RDMM_CTRL_BIT (1ull << 63)
+
+typedef struct {
+  uint32_t nranks;         /* P (FabricConfig::nranks, fabric.hpp:206) */
+  uint32_t node_group;     /* ranks per node group for byte classification */
+  uint64_t heap_bytes;     /* device heap per rank (fabric.hpp:207) */
+  uint64_t queue_capacity; /* default queue capacity (fabric.hpp:209) */
+  uint64_t ctrl_bytes;     /* control arena (0 = default 64 MiB) */
+  uint32_t first_local;    /* ranks [first_local, first_local+nlocal) */
+  uint32_t nlocal;         /*   are hosted by this process            */
+  const int* devices;      /* CUDA device of each local rank (nlocal) */
+  const char* session;     /* shm name shared by all processes; NULL or ""
+                              when every rank is local */
+} rdmm_fabric_config;
+
+int rdmm_fabric_create(const rdmm_fabric_config* cfg, rdmm_fabric** out);
+void rdmm_fabric_destroy(rdmm_fabric* f);
+uint32_t rdmm_fabric_nranks(const rdmm_fabric* f);
+uint32_t rdmm_fabric_node_group(const rdmm_fabric* f);
+uint64_t rdmm_fabric_queue_capacity(const rdmm_fabric* f);
+int rdmm_fabric_is_local(const rdmm_fabric* f, uint32_t rank);
+int rdmm_fabric_device(const rdmm_fabric* f, uint32_t rank); /* local only */
+/* Per-local-rank streams owned by the fabric: 0 = compute, 1..2 = copy. */
+rdmm_stream_t rdmm_fabric_stream(rdmm_fabric* f, uint32_t rank, int which);
+/* Mark a rank failed: wakes every barrier with RDMM_ERR_FABRIC. */
+void rdmm_fabric_abort(rdmm_fabric* f, const char* why);
+
+/* Heap (fabric.hpp:235-254, 277-360); rank must be local. */
+int rdmm_heap_alloc(rdmm_fabric* f, uint32_t rank, uint64_t nbytes,
+                    rdmm_gptr* out);
+int rdmm_heap_free(rdmm_fabric* f, rdmm_gptr p);
+int rdmm_heap_remaining(const rdmm_fabric* f, uint32_t rank, uint64_t* out);
+/* Device address of p as seen from `caller`'s GPU (local or peer-mapped);
+ * validates p against the heap (fabric.hpp:316-328). */
+int rdmm_gptr_device(rdmm_fabric* f, uint32_t caller, rdmm_gptr p,
+                     void** dev);
+
+/* One-sided transfers (fabric.hpp:436-471).  Device-side: stream-ordered
+ * copies on `stream` (NULL = the caller's copy stream 1); the handle is a
+ * CUDA event that rdmm_wait either makes `consumer` wait on (no host block)
+ * or, with consumer NULL, synchronises on the host.  Every transfer is
+ * recorded in the traffic log under the caller's phase label. */
+typedef struct {
+  void* event;
+  int error;
+} rdmm_handle;
+int rdmm_get_nb(rdmm_fabric* f, uint32_t caller, rdmm_gptr src, void* dst,
+                rdmm_stream_t stream, rdmm_handle* h);
+int rdmm_put_nb(rdmm_fabric* f, uint32_t caller, const void* src,
+                rdmm_gptr dst, rdmm_stream_t stream, rdmm_handle* h);
+int rdmm_wait(rdmm_fabric* f, rdmm_handle* h, rdmm_stream_t consumer);
+/* Blocking host-buffer forms (init / to_global / small headers). */
+int rdmm_get_host(rdmm_fabric* f, uint32_t caller, rdmm_gptr src, void* dst);
+int rdmm_put_host(rdmm_fabric* f, uint32_t caller, const void* src,
+                  rdmm_gptr dst);
+
+/* Remote atomic fetch-add on an 8-byte cell (fabric.hpp:473-487). */
+int rdmm_fetch_add_i64(rdmm_fabric* f, uint32_t caller, rdmm_gptr cell,
+                       int64_t delta, int64_t* old);
+/* Control-segment cells: `count` zeroed int64 cells owned by `owner`
+ * (WorkGrid storage, algos.hpp:103-133).  Collective over all ranks: every
+ * rank passes the same tag and receives the same base pointer. */
+int rdmm_ctrl_cells(rdmm_fabric* f, uint32_t caller, uint64_t tag,
+                    uint64_t count, rdmm_gptr* base);
+
+/* Remote queues (fabric.hpp:362-375, 502-528): MPMC push, owner-only pop,
+ * exactly-once delivery; each entry carries a GlobalPtr plus up to 40 bytes
+ * of inline header.  rdmm_queue_open is collective: every rank calls it with
+ * the same tag and gets the ids of all P queues (queue r owned by rank r). */
+int rdmm_queue_open(rdmm_fabric* f, uint32_t caller, uint64_t tag,
+                    uint64_t capacity, uint64_t* qids /* P entries */);
+int rdmm_queue_push(rdmm_fabric* f, uint32_t caller, uint64_t qid,
+                    rdmm_gptr v, const void* inl, uint32_t inl_bytes);
+/* *got = 0 when empty. */
+int rdmm_queue_pop(rdmm_fabric* f, uint32_t caller, uint64_t qid,
+                   rdmm_gptr* v, void* inl, uint32_t inl_bytes, int* got);
+/* Release control-segment storage of the collective with `tag` (queues and
+ * cells); collective. */
+int rdmm_ctrl_release(rdmm_fabric* f, uint32_t caller, uint64_t tag);
+
+/* Collective barrier over all ranks (fabric.hpp:532): first synchronises
+ * the caller's fabric streams, so device work issued before the barrier is
+ * complete and visible after it. */
+int rdmm_barrier(rdmm_fabric* f, uint32_t caller);
+
+/* Traffic log (fabric.hpp:89-203) -- phase labels, tile fetch records,
+ * per-rank event streams (Event, fabric.hpp:62-70). */
+void rdmm_set_phase(rdmm_fabric* f, uint32_t caller, int64_t label);
+int64_t rdmm_phase(rdmm_fabric* f, uint32_t caller);
+void rdmm_record_tile_fetch(rdmm_fabric* f, uint32_t caller, uint32_t owner,
+                            int matrix, uint32_t i, uint32_t j);
+void rdmm_emit_compute(rdmm_fabric* f, uint32_t caller, uint64_t flops);
+/* Record a transfer the caller satisfied without a copy (self aliasing). */
+void rdmm_record_self_get(rdmm_fabric* f, uint32_t caller, uint64_t bytes);
+typedef struct {
+  uint64_t bytes_put, bytes_got, puts, gets, atomic_ops;
+} rdmm_traffic;
+int rdmm_traffic_pair(const rdmm_fabric* f, uint32_t src, uint32_t dst,
+                      rdmm_traffic* out);
+int rdmm_traffic_total(const rdmm_fabric* f, rdmm_traffic* out);
+void rdmm_traffic_clear(rdmm_fabric* f);
+typedef struct {
+  uint32_t src, dst;
+  int64_t label;
+  int32_t matrix;
+  uint32_t i, j;
+} rdmm_tile_fetch;
+/* Copies up to cap records; returns the total count. */
+uint64_t rdmm_tile_fetches(const rdmm_fabric* f, rdmm_tile_fetch* out,
+                           uint64_t cap);
+typedef struct {
+  int32_t kind; /* 0 transfer, 1 compute, 2 queue_op */
+  uint32_t src, dst;
+  uint64_t bytes, flops;
+} rdmm_event;
+void rdmm_event_sink(rdmm_fabric* f, uint32_t caller, int enable);
+uint64_t rdmm_events(const rdmm_fabric* f, uint32_t rank, rdmm_event* out,
+                     uint64_t cap);
+
+/* Device memory helpers for the host layer (stream-ordered pool memory on
+ * the rank's GPU) so the C++ API needs no CUDA runtime of its own. */
+int rdmm_dev_alloc(rdmm_fabric* f, uint32_t rank, uint64_t bytes,
+                   rdmm_stream_t stream, void** out);
+int rdmm_dev_free(rdmm_fabric* f, uint32_t rank, void* p,
+                  rdmm_stream_t stream);
+int rdmm_memcpy(void* dst, const void* src, uint64_t bytes,
+                rdmm_stream_t stream); /* any direction; NULL stream = sync */
+int rdmm_memset(void* dst, int value, uint64_t bytes, rdmm_stream_t stream);
+int rdmm_event_record(rdmm_stream_t stream, void** event);
+int rdmm_event_query(void* event, int* done); /* done=1 when complete */
+int rdmm_event_wait(void* event, rdmm_stream_t consumer);
+int rdmm_event_sync(void* event);
+void rdmm_event_destroy(void* event);
+int rdmm_stream_sync(rdmm_stream_t stream);
+int rdmm_set_device(int device);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,6 +20,7 @@
 #include <algorithm>
 
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 
@@ -312,6 +313,110 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
+// Row-oriented variant: the worker walks the chunk row by row; each row
+// (or the chunk's slice of it) is accumulated from its own col/val window.
+template <typename T, int VEC, int G, int NV, bool CZERO, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    spmm_rows(const SpmmArgs<T> p) {
+  using V = typename VecOf<T, VEC>::type;
+  constexpr int SL = kWin / G;
+  const unsigned gm = group_mask<G>();
+  const uint32_t lane = threadIdx.x % G;
+  const uint32_t worker = (blockIdx.x * kThreads + threadIdx.x) / G;
+  const uint32_t nworkers = gridDim.x * (kThreads / G);
+  const V* __restrict__ Bv = reinterpret_cast<const V*>(p.B);
+  V* __restrict__ Cv = reinterpret_cast<V*>(p.C);
+  const uint64_t ldbv = p.ldb / VEC, ldcv = p.ldc / VEC;
+  bool colok[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) colok[v] = lane + G * v < p.nvec;
+  for (uint32_t c = worker; c < p.nchunks; c += nworkers) {
+    const uint64_t lo = uint64_t(c) * p.Q;
+    const uint64_t hi = umin(lo + p.Q, p.nnz);
+    uint32_t l = 0, h = p.rows;
+    while (h - l > 1) {
+      const uint32_t m = (l + h) >> 1;
+      if (__ldg(p.rp + m) <= lo)
+        l = m;
+      else
+        h = m;
+    }
+    uint32_t r = l;
+    uint32_t rs = __ldg(p.rp + r);
+    uint32_t re = __ldg(p.rp + r + 1);
+    int32_t trow = -1;
+    while (rs < hi) {
+      const uint32_t re_next = (r + 2 <= p.rows) ? __ldg(p.rp + r + 2) : re;
+      const uint64_t s = umax(rs, lo), e = umin(re, hi);
+      if (s < e) {
+        const bool starts = rs >= lo, ends = re <= hi;
+        V acc[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+          acc[v] = (!CZERO && starts && colok[v])
+                       ? Cv[uint64_t(r) * ldcv + lane + G * v]
+                       : vzero<V>();
+        for (uint64_t base = s; base < e; base += kWin) {
+          const uint32_t cnt = uint32_t(umin(kWin, e - base));
+          uint32_t kk[SL];
+          T aa[SL];
+#pragma unroll
+          for (int j = 0; j < SL; ++j) {
+            const uint64_t idx = base + lane + G * j;
+            const bool ok = idx < e;
+            kk[j] = ok ? __ldg(p.ci + idx) : 0u;
+            aa[j] = ok ? __ldg(p.val + idx) : T(0);
+          }
+#pragma unroll
+          for (int t = 0; t < kWin; t += kU) {
+            if (t < int(cnt)) {
+              V bv[kU][NV];
+#pragma unroll
+              for (int u = 0; u < kU; ++u) {
+                const int q = t + u;
+                const uint32_t k = __shfl_sync(gm, kk[q / G], q % G, G);
+                if (q < int(cnt)) {
+                  const V* brow = Bv + uint64_t(k) * ldbv + lane;
+#pragma unroll
+                  for (int v = 0; v < NV; ++v)
+                    if (colok[v]) bv[u][v] = __ldg(brow + G * v);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < kU; ++u) {
+                const int q = t + u;
+                const T a = __shfl_sync(gm, aa[q / G], q % G, G);
+                if (q < int(cnt)) {
+#pragma unroll
+                  for (int v = 0; v < NV; ++v)
+                    if (colok[v]) acc[v] = vfma(a, bv[u][v], acc[v]);
+                }
+              }
+            }
+          }
+        }
+        if (starts && ends) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+            if (colok[v]) Cv[uint64_t(r) * ldcv + lane + G * v] = acc[v];
+        } else {
+          V* dst = reinterpret_cast<V*>(starts ? p.tail_val : p.head_val) +
+                   uint64_t(c) * (p.wstride / VEC);
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+            if (colok[v]) dst[lane + G * v] = acc[v];
+          if (starts) trow = int32_t(r);
+        }
+      }
+      ++r;
+      rs = re;
+      re = re_next;
+      if (r >= p.rows) break;
+    }
+    if (lane == 0) p.tail_row[c] = trow;
+  }
+}
+
 // Rows cut by chunk boundaries: C[r] = tail(c) + head(c+1) + head(c+2) + ...
 template <typename T, int VEC, int G, int NV>
 __global__ void __launch_bounds__(kThreads) spmm_fixup(const SpmmArgs<T> p) {
@@ -361,19 +466,35 @@ inline int occ_variant() {
   return v;
 }
 
+// RDMM_SPMM_KERNEL=rows selects the row-oriented kernel (dev switch).
+inline int kernel_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("RDMM_SPMM_KERNEL");
+    return (e && std::string(e) == "rows") ? 1 : 0;
+  }();
+  return v;
+}
+
 template <typename T, int VEC, int G, int NV>
 void launch(const SpmmArgs<T>& a, bool czero, int blocks, int fix_blocks,
             cudaStream_t s) {
-  if (G == 32 && NV == 1 && occ_variant() == 4) {
-    if (czero)
-      spmm_stream<T, VEC, G, NV, true, 4><<<blocks, kThreads, 0, s>>>(a);
-    else
-      spmm_stream<T, VEC, G, NV, false, 4><<<blocks, kThreads, 0, s>>>(a);
+  const bool occ4 = G == 32 && NV == 1 && occ_variant() == 4;
+  if (kernel_variant() == 1) {
+    if (occ4) {
+      if (czero) spmm_rows<T, VEC, G, NV, true, 4><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_rows<T, VEC, G, NV, false, 4><<<blocks, kThreads, 0, s>>>(a);
+    } else {
+      if (czero) spmm_rows<T, VEC, G, NV, true, 1><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_rows<T, VEC, G, NV, false, 1><<<blocks, kThreads, 0, s>>>(a);
+    }
   } else {
-    if (czero)
-      spmm_stream<T, VEC, G, NV, true, 1><<<blocks, kThreads, 0, s>>>(a);
-    else
-      spmm_stream<T, VEC, G, NV, false, 1><<<blocks, kThreads, 0, s>>>(a);
+    if (occ4) {
+      if (czero) spmm_stream<T, VEC, G, NV, true, 4><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_stream<T, VEC, G, NV, false, 4><<<blocks, kThreads, 0, s>>>(a);
+    } else {
+      if (czero) spmm_stream<T, VEC, G, NV, true, 1><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_stream<T, VEC, G, NV, false, 1><<<blocks, kThreads, 0, s>>>(a);
+    }
   }
   spmm_fixup<T, VEC, G, NV><<<fix_blocks, kThreads, 0, s>>>(a);
 }
@@ -463,7 +584,7 @@ size_t workspace_bytes_impl(uint32_t rows, uint64_t nnz, uint32_t n) {
 inline int prefetch_default() {
   static const int v = [] {
     const char* e = std::getenv("RDMM_SPMM_PREFETCH");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 0;
   }();
   return v;
 }
