@@ -11,7 +11,11 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 \
            -Iinclude -I$(SRC) --expt-relaxed-constexpr -Xptxas -warn-spills
 CUDA_SRCS := $(wildcard $(SRC)/*.cu)
 CUDA_OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CUDA_SRCS))
-HDRS := $(wildcard include/*.h) $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.h)
+CXX_SRCS  := $(wildcard $(SRC)/*.cpp)
+CXX_OBJS  := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.cpp.o,$(CXX_SRCS))
+CXX       := g++
+CXXFLAGS  := -std=c++20 -O2 -g -fPIC -Wall -Wno-unused-function -Iinclude -I$(SRC) -pthread
+HDRS := $(wildcard include/*.h) $(wildcard include/rdmm/*.hpp) $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.h)
 
 all: $(LIBDIR)/librdmm_cuda.so oracle
 
@@ -19,9 +23,13 @@ $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(LIBDIR)/librdmm_cuda.so: $(CUDA_OBJS)
+$(OBJ)/%.cpp.o: $(SRC)/%.cpp $(HDRS)
+	@mkdir -p $(OBJ)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(LIBDIR)/librdmm_cuda.so: $(CUDA_OBJS) $(CXX_OBJS)
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(CUDA_OBJS) -lpthread -lrt -ldl
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(CUDA_OBJS) $(CXX_OBJS) -lpthread -lrt -ldl
 
 oracle:
 	$(MAKE) -s -C oracle

@@ -128,6 +128,8 @@ int rdmm_spgemm_symbolic(uint32_t rows, uint32_t ncols, int dtype_bytes,
 int rdmm_spgemm_numeric(rdmm_spgemm_plan* plan, uint32_t* c_col_idx,
                         void* c_val, rdmm_stream_t stream);
 void rdmm_spgemm_plan_destroy(rdmm_spgemm_plan* plan);
+/* FlopMeter flops of each term (identity terms count 0). */
+int rdmm_spgemm_plan_term_flops(const rdmm_spgemm_plan* plan, uint64_t* out);
 /* rows per symbolic / numeric tier (6 each: 5 hash tiers + dense) */
 int rdmm_spgemm_plan_info(const rdmm_spgemm_plan* plan, uint32_t* sym_tiers,
                           uint32_t* num_tiers);
@@ -141,6 +143,26 @@ int rdmm_dense_add_into_f32(uint32_t rows, uint32_t cols, float* c,
 int rdmm_dense_add_into_f64(uint32_t rows, uint32_t cols, double* c,
                             uint64_t ldc, const double* x, uint64_t ldx,
                             rdmm_stream_t stream);
+
+/* -------------------------------------------------- distributed helpers */
+/* Tile (r0.., c0..) of a device-resident global CSR (distmat.hpp:265-282):
+ * count writes out_rp (nrows+1) and returns the tile nnz (synchronises);
+ * fill copies the column-rebased indices and values. */
+int rdmm_csr_extract_count(const uint32_t* row_ptr, const uint32_t* col_idx,
+                           uint64_t r0, uint32_t nrows, uint64_t c0,
+                           uint32_t ncols, uint32_t* out_rp, uint64_t* nnz,
+                           rdmm_stream_t stream);
+int rdmm_csr_extract_fill(int dtype_bytes, const uint32_t* row_ptr,
+                          const uint32_t* col_idx, const void* val,
+                          uint64_t r0, uint32_t nrows, uint64_t c0,
+                          uint32_t ncols, const uint32_t* out_rp,
+                          uint32_t* out_ci, void* out_val,
+                          rdmm_stream_t stream);
+/* Sum of a dense tile's values in double (checksum, algos.hpp:634-669). */
+int rdmm_tile_sum(int dtype_bytes, uint32_t rows, uint32_t cols, uint64_t ld,
+                  const void* p, rdmm_stream_t stream, double* out);
+/* A single-thread kernel spinning ~ns nanoseconds (straggler injection). */
+int rdmm_spin_delay(uint64_t ns, rdmm_stream_t stream);
 
 /* ------------------------------------------------------- input generators */
 /* Device-side, bit-identical to the reference host generators (gen.hpp). */
@@ -222,6 +244,9 @@ int rdmm_fabric_is_local(const rdmm_fabric* f, uint32_t rank);
 int rdmm_fabric_device(const rdmm_fabric* f, uint32_t rank); /* local only */
 /* Per-local-rank streams owned by the fabric: 0 = compute, 1..2 = copy. */
 rdmm_stream_t rdmm_fabric_stream(rdmm_fabric* f, uint32_t rank, int which);
+/* Process-local sequence number (1, 2, ...): processes that create objects
+ * in the same order get the same numbers (collective tags). */
+uint64_t rdmm_fabric_next_uid(rdmm_fabric* f);
 /* Mark a rank failed: wakes every barrier with RDMM_ERR_FABRIC. */
 void rdmm_fabric_abort(rdmm_fabric* f, const char* why);
 
@@ -251,6 +276,8 @@ int rdmm_put_nb(rdmm_fabric* f, uint32_t caller, const void* src,
 int rdmm_wait(rdmm_fabric* f, rdmm_handle* h, rdmm_stream_t consumer);
 /* Blocking host-buffer forms (init / to_global / small headers). */
 int rdmm_get_host(rdmm_fabric* f, uint32_t caller, rdmm_gptr src, void* dst);
+/* Host read that bypasses the traffic log (Fabric::raw, fabric.hpp:251). */
+int rdmm_peek(rdmm_fabric* f, uint32_t caller, rdmm_gptr src, void* dst);
 int rdmm_put_host(rdmm_fabric* f, uint32_t caller, const void* src,
                   rdmm_gptr dst);
 
@@ -290,8 +317,11 @@ int64_t rdmm_phase(rdmm_fabric* f, uint32_t caller);
 void rdmm_record_tile_fetch(rdmm_fabric* f, uint32_t caller, uint32_t owner,
                             int matrix, uint32_t i, uint32_t j);
 void rdmm_emit_compute(rdmm_fabric* f, uint32_t caller, uint64_t flops);
-/* Record a transfer the caller satisfied without a copy (self aliasing). */
+/* Record a transfer the caller satisfied without a copy engine: a self
+ * alias, or a payload read in place over NVLink by a kernel. */
 void rdmm_record_self_get(rdmm_fabric* f, uint32_t caller, uint64_t bytes);
+void rdmm_record_get(rdmm_fabric* f, uint32_t caller, uint32_t owner,
+                     uint64_t bytes);
 typedef struct {
   uint64_t bytes_put, bytes_got, puts, gets, atomic_ops;
 } rdmm_traffic;
@@ -333,6 +363,12 @@ int rdmm_event_sync(void* event);
 void rdmm_event_destroy(void* event);
 int rdmm_stream_sync(rdmm_stream_t stream);
 int rdmm_set_device(int device);
+int rdmm_device_count(int* n);
+/* Strided 2-D copy (any direction), e.g. a dense tile out of a global array. */
+int rdmm_memcpy2d(void* dst, uint64_t dpitch, const void* src, uint64_t spitch,
+                  uint64_t width_bytes, uint64_t rows, rdmm_stream_t stream);
+/* Host address of a control-segment pointer (RDMM_CTRL_BIT set). */
+void* rdmm_ctrl_host(rdmm_fabric* f, rdmm_gptr p);
 
 #ifdef __cplusplus
 }

@@ -58,6 +58,10 @@ void* scratch(size_t bytes, int slot) {
 
 }  // namespace rdmm_impl
 
+extern "C" int rdmm_impl_fail(int code, const char* msg) {
+  return rdmm_impl::fail(code, msg ? msg : "");
+}
+
 extern "C" const char* rdmm_last_error(void) {
   return rdmm_impl::g_last_error.c_str();
 }

@@ -189,6 +189,7 @@ struct rdmm_fabric {
   std::vector<std::vector<char*>> base;
   std::vector<uint64_t> heap_bytes;  // per rank
   std::vector<std::pair<int, void*>> ipc_opened;
+  std::atomic<uint64_t> uid{0};
   mutable std::mutex tmu;
   std::map<TKey, rdmm_traffic> cells;
   std::vector<rdmm_tile_fetch> fetches;
@@ -525,6 +526,8 @@ extern "C" rdmm_stream_t rdmm_fabric_stream(rdmm_fabric* f, uint32_t rank,
   if (!L || which < 0 || which > 2) return nullptr;
   return reinterpret_cast<rdmm_stream_t>(L->streams[which]);
 }
+extern "C" uint64_t rdmm_fabric_next_uid(rdmm_fabric* f) { return ++f->uid; }
+
 extern "C" void rdmm_fabric_abort(rdmm_fabric* f, const char* why) {
   if (!f || !f->ctrl) return;
   uint32_t exp = 0;
@@ -652,6 +655,21 @@ extern "C" int rdmm_get_host(rdmm_fabric* f, uint32_t caller, rdmm_gptr src,
   if (src.length)
     RDMM_CUDA_TRY(cudaMemcpy(dst, dev_addr(f, C, src), src.length, cudaMemcpyDefault));
   f->record_get(src.rank, caller, src.length);
+  return RDMM_OK;
+}
+
+extern "C" int rdmm_peek(rdmm_fabric* f, uint32_t caller, rdmm_gptr src,
+                         void* dst) {
+  Local* C = f->local(caller);
+  if (!C) return fail(RDMM_ERR_FABRIC, "caller rank not local");
+  if (int rc = check_gptr(f, src, true)) return rc;
+  if (src.offset & RDMM_CTRL_BIT) {
+    std::memcpy(dst, f->arena + (src.offset & ~RDMM_CTRL_BIT), src.length);
+    return RDMM_OK;
+  }
+  RDMM_CUDA_TRY(cudaSetDevice(C->device));
+  if (src.length)
+    RDMM_CUDA_TRY(cudaMemcpy(dst, dev_addr(f, C, src), src.length, cudaMemcpyDefault));
   return RDMM_OK;
 }
 
@@ -836,6 +854,10 @@ extern "C" void rdmm_emit_compute(rdmm_fabric* f, uint32_t caller, uint64_t flop
 extern "C" void rdmm_record_self_get(rdmm_fabric* f, uint32_t caller, uint64_t bytes) {
   f->record_get(caller, caller, bytes);
 }
+extern "C" void rdmm_record_get(rdmm_fabric* f, uint32_t caller, uint32_t owner,
+                                uint64_t bytes) {
+  f->record_get(owner, caller, bytes);
+}
 extern "C" int rdmm_traffic_pair(const rdmm_fabric* f, uint32_t src, uint32_t dst,
                                  rdmm_traffic* out) {
   std::lock_guard<std::mutex> lk(f->tmu);
@@ -964,4 +986,27 @@ extern "C" int rdmm_stream_sync(rdmm_stream_t stream) {
 extern "C" int rdmm_set_device(int device) {
   RDMM_CUDA_TRY(cudaSetDevice(device));
   return RDMM_OK;
+}
+
+extern "C" int rdmm_device_count(int* n) {
+  RDMM_CUDA_TRY(cudaGetDeviceCount(n));
+  return RDMM_OK;
+}
+
+extern "C" int rdmm_memcpy2d(void* dst, uint64_t dpitch, const void* src,
+                             uint64_t spitch, uint64_t width_bytes,
+                             uint64_t rows, rdmm_stream_t stream) {
+  if (!rows || !width_bytes) return RDMM_OK;
+  if (stream)
+    RDMM_CUDA_TRY(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width_bytes, rows,
+                                    cudaMemcpyDefault, as_stream(stream)));
+  else
+    RDMM_CUDA_TRY(cudaMemcpy2D(dst, dpitch, src, spitch, width_bytes, rows,
+                               cudaMemcpyDefault));
+  return RDMM_OK;
+}
+
+extern "C" void* rdmm_ctrl_host(rdmm_fabric* f, rdmm_gptr p) {
+  if (!(p.offset & RDMM_CTRL_BIT)) return nullptr;
+  return f->arena + (p.offset & ~RDMM_CTRL_BIT);
 }

@@ -1,0 +1,285 @@
+// host_capi.cpp -- C-ABI over the C++ driver layer (include/rdmm/*.hpp),
+// see include/rdmm_host.h.
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <variant>
+
+#include "rdmm/algos.hpp"
+#include "rdmm_host.h"
+
+using namespace rdmm;
+
+struct rdmm_h_fabric {
+  std::unique_ptr<Fabric> f;
+};
+
+struct rdmm_h_matrix {
+  rdmm_h_fabric* fab = nullptr;
+  int kind = 0, dtype = 4;
+  std::variant<std::monostate, std::unique_ptr<DistSparse<float>>, std::unique_ptr<DistSparse<double>>,
+               std::unique_ptr<DistDense<float>>, std::unique_ptr<DistDense<double>>>
+      m;
+};
+
+namespace {
+
+int to_code(const std::exception& e) {
+  std::string msg = e.what();
+  if (dynamic_cast<const dimension_error*>(&e)) return rdmm_impl_fail(RDMM_ERR_DIMENSION, msg.c_str());
+  if (dynamic_cast<const heap_exhausted_error*>(&e)) return rdmm_impl_fail(RDMM_ERR_HEAP_EXHAUSTED, msg.c_str());
+  if (dynamic_cast<const queue_full_error*>(&e)) return rdmm_impl_fail(RDMM_ERR_QUEUE_FULL, msg.c_str());
+  if (dynamic_cast<const protocol_error*>(&e)) return rdmm_impl_fail(RDMM_ERR_PROTOCOL, msg.c_str());
+  if (dynamic_cast<const fabric_error*>(&e)) return rdmm_impl_fail(RDMM_ERR_FABRIC, msg.c_str());
+  if (dynamic_cast<const std::invalid_argument*>(&e)) return rdmm_impl_fail(RDMM_ERR_INVALID, msg.c_str());
+  return rdmm_impl_fail(RDMM_ERR_CUDA, msg.c_str());
+}
+
+template <typename F>
+int guarded(F&& fn) {
+  try {
+    fn();
+    return RDMM_OK;
+  } catch (const std::exception& e) {
+    return to_code(e);
+  } catch (...) {
+    return rdmm_impl_fail(RDMM_ERR_CUDA, "unknown exception");
+  }
+}
+
+template <typename T>
+void sparse_init(Fabric& f, DistSparse<T>& A, const uint32_t* rp, const uint32_t* ci,
+                 const void* vals, uint64_t nnz, int on_device) {
+  if (!rp) {
+    run_ranks(f, [&](RankCtx& ctx) { A.init(ctx); });
+    return;
+  }
+  if (on_device) {
+    DevCsrView<T> g{index_t(A.geom().m), index_t(A.geom().n), nnz, rp, ci,
+                    static_cast<const T*>(vals)};
+    run_ranks(f, [&](RankCtx& ctx) { A.init_from_device_global(ctx, g); });
+    return;
+  }
+  CsrTile<T> g(index_t(A.geom().m), index_t(A.geom().n));
+  g.row_ptr.assign(rp, rp + A.geom().m + 1);
+  g.col_idx.assign(ci, ci + nnz);
+  const T* v = static_cast<const T*>(vals);
+  g.values.assign(v, v + nnz);
+  run_ranks(f, [&](RankCtx& ctx) { A.init_from_global(ctx, g); });
+}
+
+template <typename T>
+void dense_init(Fabric& f, DistDense<T>& B, const void* global, uint64_t ld) {
+  if (!global) {
+    run_ranks(f, [&](RankCtx& ctx) { B.init(ctx); });
+    return;
+  }
+  run_ranks(f, [&](RankCtx& ctx) { B.init_from_host(ctx, static_cast<const T*>(global), ld); });
+}
+
+RunOptions opts_of(const rdmm_h_options* o) {
+  RunOptions r;
+  if (!o) return r;
+  r.variant = static_cast<Variant>(o->variant);
+  r.ws_base = static_cast<Variant>(o->ws_base);
+  r.prefetch = o->prefetch != 0;
+  r.offset = o->offset != 0;
+  r.seed = o->seed;
+  r.delay_ns_per_flop = o->delay_ns_per_flop;
+  r.random_delay_ms_max = o->random_delay_ms_max;
+  r.record_events = o->record_events != 0;
+  r.record_triples = o->record_triples != 0;
+  r.lookahead = o->lookahead > 0 ? o->lookahead : 2;
+  r.ws_local_inplace = o->ws_local_inplace != 0;
+  r.checksum = o->checksum != 0;
+  return r;
+}
+
+void fill(const RunReport& r, rdmm_h_report* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->wall_seconds = r.wall_seconds;
+  out->checksum = r.checksum;
+  out->total_flops = r.total_flops();
+  out->total_multiplies = r.total_multiplies();
+  out->total_steals = r.total_steals();
+  out->nranks = uint32_t(r.per_rank.size());
+  uint64_t nt = 0;
+  for (auto& t : r.triples) nt += t.size();
+  for (std::size_t p = 0; p < r.per_rank.size() && p < RDMM_H_MAX_RANKS; ++p) {
+    const auto& s = r.per_rank[p];
+    out->multiplies[p] = s.multiplies;
+    out->flops[p] = s.meter.flops;
+    out->output_nnz[p] = s.meter.output_nnz;
+    out->steals[p] = s.steals;
+    out->steals_local[p] = s.steals_with_local_component;
+    out->pushes[p] = s.queue_pushes;
+    out->pops[p] = s.queue_pops;
+    out->bytes_self[p] = s.bytes_self;
+    out->bytes_on_node[p] = s.bytes_on_node;
+    out->bytes_off_node[p] = s.bytes_off_node;
+    out->total_seconds[p] = s.total_seconds;
+  }
+  out->ntriples = nt;
+  if (nt) {
+    out->triples = static_cast<uint32_t*>(std::malloc(nt * 16));
+    uint64_t q = 0;
+    for (std::size_t p = 0; p < r.triples.size(); ++p)
+      for (auto& t : r.triples[p]) {
+        out->triples[4 * q + 0] = uint32_t(p);
+        out->triples[4 * q + 1] = t.i;
+        out->triples[4 * q + 2] = t.j;
+        out->triples[4 * q + 3] = t.k;
+        ++q;
+      }
+  }
+}
+
+template <typename T>
+void run_typed(rdmm_h_fabric* f, rdmm_h_matrix* A, rdmm_h_matrix* B, rdmm_h_matrix* C,
+               const RunOptions& o, rdmm_h_report* rep) {
+  auto& a = *std::get<std::unique_ptr<DistSparse<T>>>(A->m);
+  RunReport r;
+  if (B->kind == 1) {
+    auto& b = *std::get<std::unique_ptr<DistDense<T>>>(B->m);
+    auto& c = *std::get<std::unique_ptr<DistDense<T>>>(C->m);
+    r = run_multiply(*f->f, a, b, c, o);
+  } else {
+    auto& b = *std::get<std::unique_ptr<DistSparse<T>>>(B->m);
+    auto& c = *std::get<std::unique_ptr<DistSparse<T>>>(C->m);
+    r = run_multiply(*f->f, a, b, c, o);
+  }
+  fill(r, rep);
+}
+
+}  // namespace
+
+extern "C" int rdmm_h_fabric_create(uint32_t nranks, uint64_t heap_bytes, uint32_t node_group,
+                                    uint64_t queue_capacity, uint32_t first_local,
+                                    uint32_t nlocal, const int* devices, const char* session,
+                                    rdmm_h_fabric** out) {
+  *out = nullptr;
+  return guarded([&] {
+    FabricConfig c;
+    c.nranks = nranks;
+    c.heap_bytes = heap_bytes;
+    c.node_group = node_group ? node_group : 6;
+    c.queue_capacity = queue_capacity ? queue_capacity : 4096;
+    c.first_local = first_local;
+    c.nlocal = nlocal;
+    if (devices) c.devices.assign(devices, devices + (nlocal ? nlocal : nranks));
+    if (session) c.session = session;
+    auto h = std::make_unique<rdmm_h_fabric>();
+    h->f = std::make_unique<Fabric>(c);
+    *out = h.release();
+  });
+}
+
+extern "C" void rdmm_h_fabric_destroy(rdmm_h_fabric* f) { delete f; }
+extern "C" void* rdmm_h_fabric_handle(rdmm_h_fabric* f) { return f->f->handle(); }
+
+extern "C" int rdmm_h_matrix_create(rdmm_h_fabric* f, int kind, int dtype, uint64_t m, uint64_t n,
+                                    uint32_t tm, uint32_t tn, uint32_t pr, uint32_t pc,
+                                    int matrix_id, rdmm_h_matrix** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto h = std::make_unique<rdmm_h_matrix>();
+    h->fab = f;
+    h->kind = kind;
+    h->dtype = dtype;
+    ProcGrid g{pr, pc};
+    if (kind == 0 && dtype == 8)
+      h->m = std::make_unique<DistSparse<double>>(*f->f, m, n, tm, tn, g, matrix_id);
+    else if (kind == 0)
+      h->m = std::make_unique<DistSparse<float>>(*f->f, m, n, tm, tn, g, matrix_id);
+    else if (dtype == 8)
+      h->m = std::make_unique<DistDense<double>>(*f->f, m, n, tm, tn, g, matrix_id);
+    else
+      h->m = std::make_unique<DistDense<float>>(*f->f, m, n, tm, tn, g, matrix_id);
+    *out = h.release();
+  });
+}
+
+extern "C" void rdmm_h_matrix_destroy(rdmm_h_matrix* mat) { delete mat; }
+
+extern "C" int rdmm_h_sparse_init(rdmm_h_matrix* mat, const uint32_t* rp, const uint32_t* ci,
+                                  const void* vals, uint64_t nnz, int on_device) {
+  return guarded([&] {
+    if (mat->kind != 0) throw std::invalid_argument("not a sparse matrix");
+    if (mat->dtype == 8)
+      sparse_init(*mat->fab->f, *std::get<std::unique_ptr<DistSparse<double>>>(mat->m), rp, ci,
+                  vals, nnz, on_device);
+    else
+      sparse_init(*mat->fab->f, *std::get<std::unique_ptr<DistSparse<float>>>(mat->m), rp, ci,
+                  vals, nnz, on_device);
+  });
+}
+
+extern "C" int rdmm_h_dense_init(rdmm_h_matrix* mat, const void* global, uint64_t ld) {
+  return guarded([&] {
+    if (mat->kind != 1) throw std::invalid_argument("not a dense matrix");
+    if (mat->dtype == 8)
+      dense_init(*mat->fab->f, *std::get<std::unique_ptr<DistDense<double>>>(mat->m), global, ld);
+    else
+      dense_init(*mat->fab->f, *std::get<std::unique_ptr<DistDense<float>>>(mat->m), global, ld);
+  });
+}
+
+extern "C" int rdmm_h_dense_to_host(rdmm_h_matrix* mat, void* out) {
+  return guarded([&] {
+    if (mat->dtype == 8) {
+      auto g = std::get<std::unique_ptr<DistDense<double>>>(mat->m)->to_global();
+      std::memcpy(out, g.data(), g.size() * 8);
+    } else {
+      auto g = std::get<std::unique_ptr<DistDense<float>>>(mat->m)->to_global();
+      std::memcpy(out, g.data(), g.size() * 4);
+    }
+  });
+}
+
+extern "C" int rdmm_h_sparse_nnz(rdmm_h_matrix* mat, uint64_t* nnz) {
+  return guarded([&] {
+    uint64_t n = 0;
+    auto count = [&](auto& A) {
+      for (uint32_t i = 0; i < A.tile_grid_rows(); ++i)
+        for (uint32_t j = 0; j < A.tile_grid_cols(); ++j) n += A.tile_nnz(i, j);
+    };
+    if (mat->dtype == 8)
+      count(*std::get<std::unique_ptr<DistSparse<double>>>(mat->m));
+    else
+      count(*std::get<std::unique_ptr<DistSparse<float>>>(mat->m));
+    *nnz = n;
+  });
+}
+
+extern "C" int rdmm_h_sparse_to_host(rdmm_h_matrix* mat, uint32_t* rp, uint32_t* ci,
+                                     void* vals) {
+  return guarded([&] {
+    auto out = [&](auto g) {
+      std::memcpy(rp, g.row_ptr.data(), g.row_ptr.size() * 4);
+      std::memcpy(ci, g.col_idx.data(), g.col_idx.size() * 4);
+      std::memcpy(vals, g.values.data(), g.values.size() * sizeof(g.values[0]));
+    };
+    if (mat->dtype == 8)
+      out(std::get<std::unique_ptr<DistSparse<double>>>(mat->m)->to_global());
+    else
+      out(std::get<std::unique_ptr<DistSparse<float>>>(mat->m)->to_global());
+  });
+}
+
+extern "C" int rdmm_h_run_multiply(rdmm_h_fabric* f, rdmm_h_matrix* A, rdmm_h_matrix* B,
+                                   rdmm_h_matrix* C, const rdmm_h_options* o,
+                                   rdmm_h_report* rep) {
+  return guarded([&] {
+    if (A->kind != 0) throw std::invalid_argument("A must be sparse");
+    if (B->kind != C->kind) throw std::invalid_argument("B and C must be both dense or sparse");
+    if (A->dtype != B->dtype || A->dtype != C->dtype) throw std::invalid_argument("dtype mismatch");
+    const RunOptions ro = opts_of(o);
+    if (A->dtype == 8)
+      run_typed<double>(f, A, B, C, ro, rep);
+    else
+      run_typed<float>(f, A, B, C, ro, rep);
+  });
+}
+
+extern "C" void rdmm_h_free(void* p) { std::free(p); }

@@ -24,6 +24,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -170,11 +171,17 @@ __device__ __forceinline__ void enumerate_row(uint32_t r,
 
 // ------------------------------------------------------------ binning
 
-// Warp per row: ub[r] = number of products; bin by symbolic tier.
+// Warp per row: ub[r] = number of products; bin by symbolic tier.  Per-term
+// product counts (the reference FlopMeter per multiply, tile.hpp:197-209) are
+// reduced in shared memory and flushed with one global atomic per term per
+// block.
 template <typename T>
 __global__ void k_bin_sym(uint32_t rows, const TermDev<T>* terms, int nterms,
                           uint32_t* lists, uint32_t* tier_count,
-                          unsigned long long* total_ub, uint64_t* cnt64) {
+                          unsigned long long* term_products, uint64_t* cnt64) {
+  extern __shared__ unsigned long long sacc[];
+  for (int t = threadIdx.x; t < nterms; t += blockDim.x) sacc[t] = 0;
+  __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -182,22 +189,24 @@ __global__ void k_bin_sym(uint32_t rows, const TermDev<T>* terms, int nterms,
     unsigned long long ub = 0;
     for (int t = 0; t < nterms; ++t) {
       const TermDev<T> tm = terms[t];
+      unsigned long long tp = 0;
       if (tm.arp == nullptr) {
-        if (lane == 0) ub += __ldg(tm.brp + r + 1) - __ldg(tm.brp + r);
-        continue;
+        if (lane == 0) tp = __ldg(tm.brp + r + 1) - __ldg(tm.brp + r);
+      } else {
+        const uint32_t s0 = __ldg(tm.arp + r), s1 = __ldg(tm.arp + r + 1);
+        for (uint32_t e = s0 + lane; e < s1; e += 32) {
+          const uint32_t k = __ldg(tm.aci + e);
+          tp += __ldg(tm.brp + k + 1) - __ldg(tm.brp + k);
+        }
       }
-      const uint32_t s0 = __ldg(tm.arp + r), s1 = __ldg(tm.arp + r + 1);
-      for (uint32_t e = s0 + lane; e < s1; e += 32) {
-        const uint32_t k = __ldg(tm.aci + e);
-        ub += __ldg(tm.brp + k + 1) - __ldg(tm.brp + k);
-      }
-    }
 #pragma unroll
-    for (int off = 16; off; off >>= 1) ub += __shfl_xor_sync(0xffffffffu, ub, off);
+      for (int off = 16; off; off >>= 1) tp += __shfl_xor_sync(0xffffffffu, tp, off);
+      if (lane == 0 && tp && tm.arp != nullptr) atomicAdd(sacc + t, tp);
+      ub += tp;
+    }
     if (lane == 0) {
       cnt64[r] = 0;
       if (ub) {
-        atomicAdd(total_ub, ub);
         int tier = 5;
         for (int i = 0; i < 5; ++i)
           if (ub <= sym_limit(i)) {
@@ -209,6 +218,9 @@ __global__ void k_bin_sym(uint32_t rows, const TermDev<T>* terms, int nterms,
       }
     }
   }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nterms; t += blockDim.x)
+    if (sacc[t]) atomicAdd(term_products + t, sacc[t]);
 }
 
 __global__ void k_bin_num(uint32_t rows, const uint64_t* cnt64, uint32_t* lists,
@@ -499,6 +511,7 @@ struct rdmm_spgemm_plan {
   Buf terms, cnt64, pre64, lists, tcount, ub, scan_tmp, bitmaps, dense;
   uint32_t sym_count[kTiers] = {0}, num_count[kTiers] = {0};
   uint64_t nnz = 0, flops = 0;
+  std::vector<uint64_t> term_flops;
   uint32_t* c_row_ptr = nullptr;
 };
 
@@ -536,8 +549,9 @@ int symbolic_impl(uint32_t rows, uint32_t ncols, const rdmm_spgemm_term* terms,
   RDMM_CUDA_TRY(P->cnt64.ensure(sizeof(uint64_t) * (size_t(rows) + 1)));
   RDMM_CUDA_TRY(P->pre64.ensure(sizeof(uint64_t) * (size_t(rows) + 1)));
   RDMM_CUDA_TRY(P->lists.ensure(sizeof(uint32_t) * size_t(kTiers) * (rows ? rows : 1)));
-  RDMM_CUDA_TRY(P->tcount.ensure(sizeof(uint32_t) * 2 * kTiers + 16));
-  RDMM_CUDA_TRY(cudaMemsetAsync(P->tcount.p, 0, sizeof(uint32_t) * 2 * kTiers + 16, s));
+  const size_t tc_bytes = sizeof(uint32_t) * 2 * kTiers + 8 * size_t(nterms) + 16;
+  RDMM_CUDA_TRY(P->tcount.ensure(tc_bytes));
+  RDMM_CUDA_TRY(cudaMemsetAsync(P->tcount.p, 0, tc_bytes, s));
   RDMM_CUDA_TRY(cudaMemsetAsync(P->cnt64.p, 0, sizeof(uint64_t) * (size_t(rows) + 1), s));
   uint32_t* tc = P->tcount.as<uint32_t>();
   auto* tub = reinterpret_cast<unsigned long long*>(tc + 2 * kTiers);
@@ -547,14 +561,23 @@ int symbolic_impl(uint32_t rows, uint32_t ncols, const rdmm_spgemm_term* terms,
   if (rows && nterms) {
     const unsigned blocks = unsigned(std::min<uint64_t>(
         ceil_div(rows, 8), uint64_t(num_sms()) * 16));
-    k_bin_sym<T><<<blocks, 256, 0, s>>>(rows, td, nterms, lists, tc, tub, cnt);
+    k_bin_sym<T><<<blocks, 256, 8 * size_t(nterms), s>>>(rows, td, nterms, lists,
+                                                         tc, tub, cnt);
     RDMM_CUDA_TRY(cudaGetLastError());
   }
-  uint32_t hc[2 * kTiers + 4];
-  RDMM_CUDA_TRY(cudaMemcpyAsync(hc, tc, sizeof(hc), cudaMemcpyDeviceToHost, s));
+  std::vector<uint32_t> hcv(2 * kTiers + 2 * size_t(nterms) + 4);
+  uint32_t* hc = hcv.data();
+  RDMM_CUDA_TRY(cudaMemcpyAsync(hc, tc, tc_bytes - 16 + 8, cudaMemcpyDeviceToHost, s));
   RDMM_CUDA_TRY(cudaStreamSynchronize(s));
   for (int i = 0; i < kTiers; ++i) P->sym_count[i] = hc[i];
-  P->flops = 2 * *reinterpret_cast<unsigned long long*>(hc + 2 * kTiers);
+  P->term_flops.assign(nterms, 0);
+  P->flops = 0;
+  for (int t = 0; t < nterms; ++t) {
+    uint64_t v;
+    std::memcpy(&v, hc + 2 * kTiers + 2 * t, 8);
+    P->term_flops[t] = 2 * v;
+    P->flops += 2 * v;
+  }
   auto L = [&](int tier) { return lists + size_t(tier) * rows; };
   int rc = 0;
   rc |= launch_sym_hash<T, 64, 32>(L(0), hc[0], td, nterms, cnt, s);
@@ -676,6 +699,13 @@ extern "C" int rdmm_spgemm_numeric(rdmm_spgemm_plan* plan, uint32_t* c_col_idx,
 }
 
 extern "C" void rdmm_spgemm_plan_destroy(rdmm_spgemm_plan* plan) { delete plan; }
+
+extern "C" int rdmm_spgemm_plan_term_flops(const rdmm_spgemm_plan* plan,
+                                           uint64_t* out) {
+  if (!plan) return fail(RDMM_ERR_INVALID, "spgemm: null plan");
+  for (size_t t = 0; t < plan->term_flops.size(); ++t) out[t] = plan->term_flops[t];
+  return RDMM_OK;
+}
 
 extern "C" int rdmm_spgemm_plan_info(const rdmm_spgemm_plan* plan,
                                      uint32_t* sym_tiers, uint32_t* num_tiers) {

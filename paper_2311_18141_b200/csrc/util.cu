@@ -1,0 +1,163 @@
+// util.cu -- device helpers behind the distributed-matrix layer:
+//   tile extraction from a device-resident global CSR (distmat.hpp:265-282),
+//   per-tile value sums for the order-insensitive checksum
+//   (algos.hpp:634-669), and the injected straggler delay (algos.hpp:212-220).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace rdmm_impl {
+namespace {
+
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a,
+                                                    uint32_t lo, uint32_t hi,
+                                                    uint64_t key) {
+  while (lo < hi) {
+    const uint32_t m = (lo + hi) >> 1;
+    if (uint64_t(a[m]) < key)
+      lo = m + 1;
+    else
+      hi = m;
+  }
+  return lo;
+}
+
+// count of row r's columns inside [c0, c1)
+__global__ void k_extract_count(const uint32_t* rp, const uint32_t* ci,
+                                uint64_t r0, uint32_t nrows, uint64_t c0,
+                                uint64_t c1, uint32_t* cnt) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
+       r += gridDim.x * blockDim.x) {
+    const uint32_t s = rp[r0 + r], e = rp[r0 + r + 1];
+    const uint32_t a = lower_bound_u32(ci, s, e, c0);
+    const uint32_t b = lower_bound_u32(ci, a, e, c1);
+    cnt[r] = b - a;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt[nrows] = 0;
+}
+
+template <typename T>
+__global__ void k_extract_fill(const uint32_t* rp, const uint32_t* ci,
+                               const T* val, uint64_t r0, uint32_t nrows,
+                               uint64_t c0, uint64_t c1,
+                               const uint32_t* out_rp, uint32_t* out_ci,
+                               T* out_val) {
+  // a warp per row: coalesced copy of the row's in-range slice
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = w; r < nrows; r += nw) {
+    const uint32_t s = rp[r0 + r], e = rp[r0 + r + 1];
+    const uint32_t a = lower_bound_u32(ci, s, e, c0);
+    const uint32_t o = out_rp[r], n = out_rp[r + 1] - o;
+    for (uint32_t q = lane; q < n; q += 32) {
+      out_ci[o + q] = uint32_t(ci[a + q] - c0);
+      out_val[o + q] = val[a + q];
+    }
+  }
+  (void)c1;
+}
+
+template <typename T>
+__global__ void k_tile_sum(uint32_t rows, uint32_t cols, uint64_t ld,
+                           const T* p, double* out) {
+  double s = 0;
+  const uint64_t total = uint64_t(rows) * cols;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    s += double(p[(i / cols) * ld + i % cols]);
+  typedef cub::BlockReduce<double, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  s = BR(tmp).Sum(s);
+  if (threadIdx.x == 0) atomicAdd(out, s);
+}
+
+__global__ void k_spin(unsigned long long ns) {
+  const unsigned long long t0 = clock64();
+  // clock64 runs at the SM clock (~1.9 GHz); spin ~ns nanoseconds
+  while (clock64() - t0 < ns * 2) {
+  }
+}
+
+}  // namespace
+}  // namespace rdmm_impl
+
+using namespace rdmm_impl;
+
+extern "C" int rdmm_csr_extract_count(const uint32_t* rp, const uint32_t* ci,
+                                      uint64_t r0, uint32_t nrows, uint64_t c0,
+                                      uint32_t ncols, uint32_t* out_rp,
+                                      uint64_t* nnz, rdmm_stream_t stream) {
+  cudaStream_t s = as_stream(stream);
+  void* cnt = scratch(4ull * (nrows + 1), 1);
+  if (!cnt) return fail(RDMM_ERR_CUDA, "extract: scratch allocation failed");
+  const unsigned blocks = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>(ceil_div(nrows, 256), uint64_t(num_sms()) * 8)));
+  k_extract_count<<<blocks, 256, 0, s>>>(rp, ci, r0, nrows, c0, c0 + ncols,
+                                         static_cast<uint32_t*>(cnt));
+  size_t tb = 0;
+  RDMM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, static_cast<uint32_t*>(cnt),
+                                              out_rp, int64_t(nrows) + 1, s));
+  void* tmp = scratch(tb + 16, 2);
+  if (!tmp) return fail(RDMM_ERR_CUDA, "extract: scratch allocation failed");
+  RDMM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, static_cast<uint32_t*>(cnt),
+                                              out_rp, int64_t(nrows) + 1, s));
+  uint32_t n = 0;
+  RDMM_CUDA_TRY(cudaMemcpyAsync(&n, out_rp + nrows, 4, cudaMemcpyDeviceToHost, s));
+  RDMM_CUDA_TRY(cudaStreamSynchronize(s));
+  *nnz = n;
+  return RDMM_OK;
+}
+
+extern "C" int rdmm_csr_extract_fill(int dtype_bytes, const uint32_t* rp,
+                                     const uint32_t* ci, const void* val,
+                                     uint64_t r0, uint32_t nrows, uint64_t c0,
+                                     uint32_t ncols, const uint32_t* out_rp,
+                                     uint32_t* out_ci, void* out_val,
+                                     rdmm_stream_t stream) {
+  cudaStream_t s = as_stream(stream);
+  const unsigned blocks = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>(ceil_div(nrows, 8), uint64_t(num_sms()) * 16)));
+  if (dtype_bytes == 8)
+    k_extract_fill<double><<<blocks, 256, 0, s>>>(
+        rp, ci, static_cast<const double*>(val), r0, nrows, c0, c0 + ncols,
+        out_rp, out_ci, static_cast<double*>(out_val));
+  else
+    k_extract_fill<float><<<blocks, 256, 0, s>>>(
+        rp, ci, static_cast<const float*>(val), r0, nrows, c0, c0 + ncols,
+        out_rp, out_ci, static_cast<float*>(out_val));
+  RDMM_CUDA_TRY(cudaGetLastError());
+  return RDMM_OK;
+}
+
+extern "C" int rdmm_tile_sum(int dtype_bytes, uint32_t rows, uint32_t cols,
+                             uint64_t ld, const void* p, rdmm_stream_t stream,
+                             double* out) {
+  cudaStream_t s = as_stream(stream);
+  double* d = static_cast<double*>(scratch(64, 3));
+  if (!d) return fail(RDMM_ERR_CUDA, "tile_sum: scratch allocation failed");
+  RDMM_CUDA_TRY(cudaMemsetAsync(d, 0, 8, s));
+  const uint64_t total = uint64_t(rows) * cols;
+  if (total) {
+    const unsigned blocks = unsigned(std::max<uint64_t>(
+        1, std::min<uint64_t>(ceil_div(total, 256), uint64_t(num_sms()) * 4)));
+    if (dtype_bytes == 8)
+      k_tile_sum<double><<<blocks, 256, 0, s>>>(rows, cols, ld,
+                                                static_cast<const double*>(p), d);
+    else
+      k_tile_sum<float><<<blocks, 256, 0, s>>>(rows, cols, ld,
+                                               static_cast<const float*>(p), d);
+  }
+  RDMM_CUDA_TRY(cudaMemcpyAsync(out, d, 8, cudaMemcpyDeviceToHost, s));
+  RDMM_CUDA_TRY(cudaStreamSynchronize(s));
+  return RDMM_OK;
+}
+
+extern "C" int rdmm_spin_delay(uint64_t ns, rdmm_stream_t stream) {
+  if (!ns) return RDMM_OK;
+  k_spin<<<1, 1, 0, as_stream(stream)>>>(ns);
+  RDMM_CUDA_TRY(cudaGetLastError());
+  return RDMM_OK;
+}
