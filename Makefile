@@ -17,7 +17,7 @@ CXX       := g++
 CXXFLAGS  := -std=c++20 -O2 -g -fPIC -Wall -Wno-unused-function -Iinclude -I$(SRC) -pthread
 HDRS := $(wildcard include/*.h) $(wildcard include/rdmm/*.hpp) $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.h)
 
-all: $(LIBDIR)/librdmm_cuda.so oracle
+all: $(LIBDIR)/librdmm_cuda.so oracle build/tests/test_api
 
 $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)
@@ -30,6 +30,12 @@ $(OBJ)/%.cpp.o: $(SRC)/%.cpp $(HDRS)
 $(LIBDIR)/librdmm_cuda.so: $(CUDA_OBJS) $(CXX_OBJS)
 	@mkdir -p $(LIBDIR)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(CUDA_OBJS) $(CXX_OBJS) -lpthread -lrt -ldl
+
+# C++ drop-in API test program (run on the GPU by tests/test_cpp_gpu.py)
+build/tests/test_api: tests/cpp/test_api.cpp $(LIBDIR)/librdmm_cuda.so $(HDRS)
+	@mkdir -p build/tests
+	$(CXX) -std=c++20 -O1 -g -Iinclude -pthread -o $@ tests/cpp/test_api.cpp \
+	    -L$(LIBDIR) -lrdmm_cuda -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)'
 
 oracle:
 	$(MAKE) -s -C oracle

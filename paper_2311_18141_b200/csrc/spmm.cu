@@ -456,21 +456,22 @@ struct Plan {
   uint64_t Q = 0;
 };
 
-// RDMM_SPMM_OCC=4 selects the 64-register (4 CTAs/SM) build of the main
-// kernel; default is the unconstrained build.
+// RDMM_SPMM_OCC=1|4 forces the unconstrained / 64-register (4 CTAs/SM)
+// build of the main kernel (dev switch; default auto).
 inline int occ_variant() {
   static const int v = [] {
     const char* e = std::getenv("RDMM_SPMM_OCC");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 0;
   }();
   return v;
 }
 
-// RDMM_SPMM_KERNEL=rows selects the row-oriented kernel (dev switch).
+// RDMM_SPMM_KERNEL=rows|stream forces a kernel (dev switch; default auto).
 inline int kernel_variant() {
   static const int v = [] {
     const char* e = std::getenv("RDMM_SPMM_KERNEL");
-    return (e && std::string(e) == "rows") ? 1 : 0;
+    if (!e) return 0;  // auto
+    return std::string(e) == "rows" ? 1 : 2;
   }();
   return v;
 }
@@ -478,8 +479,15 @@ inline int kernel_variant() {
 template <typename T, int VEC, int G, int NV>
 void launch(const SpmmArgs<T>& a, bool czero, int blocks, int fix_blocks,
             cudaStream_t s) {
-  const bool occ4 = G == 32 && NV == 1 && occ_variant() == 4;
-  if (kernel_variant() == 1) {
+  // Measured on B200 (profiles/): the nnz-stream kernel at
+  // 64 registers (4 CTAs/SM) wins for one 16-B vector per lane (N=128 fp32);
+  // wider rows (NV>=2) keep more gathers in flight per lane and the
+  // row-oriented kernel is faster there (at the HBM gather roofline on ER).
+  const int kv = kernel_variant();
+  const bool use_rows = kv == 1 || (kv == 0 && !(G == 32 && NV == 1));
+  const int ov = occ_variant();
+  const bool occ4 = G == 32 && NV == 1 && (ov == 4 || (ov == 0 && !use_rows));
+  if (use_rows) {
     if (occ4) {
       if (czero) spmm_rows<T, VEC, G, NV, true, 4><<<blocks, kThreads, 0, s>>>(a);
       else spmm_rows<T, VEC, G, NV, false, 4><<<blocks, kThreads, 0, s>>>(a);
