@@ -1,14 +1,19 @@
 #!/usr/bin/env python
-"""Benchmark driver (see DESIGN.md §5 for the measurement contract).
+"""Benchmark driver (measurement contract: DESIGN.md §5).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3]
-    python bench.py --impl reference ...      # the reference CPU path
+                    [--variant stationary_c|ws_locality|...|summa_nccl]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU)
+    python bench.py --impl reference ...                  (reference CPU path)
 
-One JSON line on stdout (rank 0).  A "step" is one pass of the hot path over
-one synthetic input of BASELINE.json's configuration: for SpMM, C += A*B with
-A = R-MAT (or Erdos-Renyi) CSR and B dense fp32, everything resident in HBM
-when the timed region starts.  `e2e` repeats the step through the public API
-from pinned HOST buffers (H2D of A and B, D2H of C inside the timed region).
+Prints ONE JSON line (rank 0).  A step is one distributed multiply
+C = A*B of BASELINE.json's configuration through the reference entry point
+run_multiply (one process per GPU, the one-sided fabric over NVLink), C
+reset to zero (SpMM) / empty (SpGEMM) before each step outside the timed
+region, inputs resident in HBM.  `value` = total useful GFLOP/s over all
+ranks (max-over-ranks device time).  `e2e` repeats the step through the
+public API from pinned HOST buffers (upload of A and of the rank's B tiles,
+download of the rank's C tiles inside the timed region).
 """
 from __future__ import annotations
 
@@ -19,7 +24,6 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -59,9 +63,7 @@ class ClockSampler:
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int):
-        self.gpu = gpu
-        self.proc = None
-        self.path = None
+        self.gpu, self.proc, self.path = gpu, None, None
 
     def __enter__(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
@@ -105,11 +107,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
-def spmm_bytes(m, k, n, nnz, w=4):
-    """Compulsory bytes: 4(m+1) + (w+4) nnz + w k n + w m n."""
-    return 4 * (m + 1) + (w + 4) * nnz + w * k * n + w * m * n
-
-
 def row_sample(rp, ci, vv, stride):
     """Every `stride`-th row of a host CSR (keeps the degree distribution)."""
     import numpy as np
@@ -124,18 +121,40 @@ def row_sample(rp, ci, vv, stride):
     return nrp, ci[keep], vv[keep]
 
 
-def load_traffic(config, kernel):
+def load_traffic(config, kernel, n_gpus):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(config, {}).get(kernel)
+            return json.load(f).get(f"{config}@{n_gpus}", {}).get(kernel)
     except Exception:
         return None
+
+
+def layout(cfg, P, args):
+    """ProcGrid and tile sizes for P ranks.
+
+    SpMM: a 1 x P grid (B and C split by columns, K = P column tiles of A)
+    keeps every rank's compute identical and moves only A tiles (SURVEY
+    §8(e)).  SpGEMM: a P x 1 grid with 4P row tiles of C and K = P, so the
+    locality-aware work stealing can rebalance R-MAT's row skew.
+    """
+    n_rows = 1 << cfg["scale"]
+    if args.grid:
+        pr, pc = (int(x) for x in args.grid.split("x"))
+    elif cfg["kind"] == "spmm":
+        pr, pc = 1, P
+    else:
+        pr, pc = P, 1
+    mt = args.mtiles or (pr if cfg["kind"] == "spmm" else 4 * pr)
+    kt = args.ktiles or (pc if cfg["kind"] == "spmm" else pr)
+    ncols = cfg["n"] if cfg["kind"] == "spmm" else n_rows
+    nt = args.ntiles or pc
+    return (pr, pc), (-(-n_rows // mt), -(-n_rows // kt), -(-ncols // nt))
 
 
 # ----------------------------------------------------------------- our arm
 
 
-def make_spmm_inputs(cfg, dev):
+def gen_inputs(cfg, dev):
     import paper_2311_18141_b200 as rd
     import torch
 
@@ -144,90 +163,197 @@ def make_spmm_inputs(cfg, dev):
     else:
         n = 1 << cfg["scale"]
         a = rd.uniform_tiles(n, n, 1, cfg["d"], 1, device=dev)
-    b = rd.random_dense(a.cols, cfg["n"], 2, device=dev)
-    c = torch.zeros((a.rows, cfg["n"]), dtype=torch.float32, device=dev)
+    b = rd.random_dense(a.cols, cfg["n"], 2, device=dev) if cfg["kind"] == "spmm" else None
     torch.cuda.synchronize()
-    return a, b, c
+    return a, b
 
 
-def cpu_baseline_spmm(a, b, cfg_name):
-    """Reference spmm_local (oracle/_ref, else the C port) on the host, 1 core."""
-    import numpy as np
-
+def cpu_baseline(a, b, cfg):
+    """Reference spmm_local / spgemm_local (oracle/_ref = the unmodified
+    reference headers; else the C port) on this host, 1 core, bounded
+    sample: every S-th row of A."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
     import oracle
 
     impl, kind = (oracle.ref(), "reference") if oracle.ref_available() else (oracle.port(), "port")
     rp, ci, vv = a.to_host()
-    bh = b.cpu().numpy()
-    # bounded sample: a strided subset of rows (keeps the R-MAT degree mix)
-    stride = 1 if cfg_name in ("cfg1",) else 4
-    nrp, nci, nvv = row_sample(rp, ci, vv, stride)
-    h = oracle.Csr(len(nrp) - 1, a.cols, nrp, nci, nvv)
-    rows = np.arange(h.rows)
-    c = np.zeros((h.rows, bh.shape[1]), np.float32)
-    t0 = time.perf_counter()
-    fl = impl.spmm_local(h, bh, c)
-    dt = time.perf_counter() - t0
+    if cfg["kind"] == "spmm":
+        bh = b.cpu().numpy()
+        stride = 1 if a.nnz < 5_000_000 else 4
+        nrp, nci, nvv = row_sample(rp, ci, vv, stride)
+        h = oracle.Csr(len(nrp) - 1, a.cols, nrp, nci, nvv)
+        c = np.zeros((h.rows, bh.shape[1]), np.float32)
+        t0 = time.perf_counter()
+        fl = impl.spmm_local(h, bh, c)
+        dt = time.perf_counter() - t0
+        what = "spmm_local"
+    else:
+        stride = 16 if a.nnz < 2_000_000 else 256
+        nrp, nci, nvv = row_sample(rp, ci, vv, stride)
+        h = oracle.Csr(len(nrp) - 1, a.cols, nrp, nci, nvv)
+        full = oracle.Csr(a.rows, a.cols, rp, ci, vv)
+        t0 = time.perf_counter()
+        _, fl = impl.spgemm_local(h, full)
+        dt = time.perf_counter() - t0
+        what = "spgemm_local"
     return {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": kind,
-            "sample": f"spmm_local over every {stride}th row of A ({len(rows)} rows, "
-                      f"{h.nnz} nnz, {fl} flop) x full B, 1 thread, {dt:.2f} s"}
+            "sample": f"{what} over every {stride}th row of A ({h.rows} rows, {h.nnz} nnz, "
+                      f"{fl} flop), 1 thread, {dt:.2f} s"}
 
 
-def run_spmm_local(args, cfg, dev, rank, world):
-    """N=1 (or per-rank replica) local path: one spmm_local per step."""
-    import paper_2311_18141_b200 as rd
+def make_session(world, rank):
+    if world == 1:
+        return None
+    import torch.distributed as dist
+
+    obj = [f"b{os.getpid()}_{time.time_ns() % 10**9}" if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def run_ours(args, cfg, dev, rank, world):
     import torch
+    import paper_2311_18141_b200 as rd
+    import paper_2311_18141_b200.dist as dm
+    from paper_2311_18141_b200 import _lib as L
 
-    a, b, c = make_spmm_inputs(cfg, dev)
-    m, k, n, nnz = a.rows, a.cols, cfg["n"], a.nnz
-    flops = 2 * nnz * n
-    stream = torch.cuda.current_stream()
+    tdist = torch.distributed if world > 1 else None
+    a, b = gen_inputs(cfg, dev)
+    m, k, nnz_a = a.rows, a.cols, a.nnz
+    n = cfg["n"] if cfg["kind"] == "spmm" else a.cols
+    (pr, pc), (tm, tk, tn) = layout(cfg, world, args)
+    grid = dm.ProcGrid(pr, pc)
+    session = make_session(world, rank)
+    a_bytes = nnz_a * 8 + (m + 1) * 4
+    if cfg["kind"] == "spmm":
+        heap = int(2 * (a_bytes + 4 * (k * n + m * n)) / world) + (1 << 30)
+    else:
+        heap = int(4 * a_bytes) + (14 << 30) // world + (2 << 30)
+    f = dm.Fabric(nranks=world, heap_bytes=heap, first_local=rank, nlocal=1,
+                  devices=[dev.index], session=session)
+    A = dm.DistSparse(f, m, k, tm, tk, grid, 0)
+    if cfg["kind"] == "spmm":
+        B = dm.DistDense(f, k, n, tk, tn, grid, 1)
+        Cm = dm.DistDense(f, m, n, tm, tn, grid, 2)
+        A.init_from_device(a)
+        B.init_from_device(b)
+        Cm.init()
+        reset = Cm.zero
+    else:
+        B = dm.DistSparse(f, k, n, tk, tn, grid, 1)
+        Cm = dm.DistSparse(f, m, n, tm, tn, grid, 2)
+        A.init_from_device(a)
+        B.init_from_device(a)
+        Cm.init()
+        reset = Cm.init
+    variant = args.variant
+    opts = dict(variant=variant, ws_base="stationary_c", checksum=False, record_events=False)
+    stream = torch.cuda.ExternalStream(f.stream(rank), device=dev)
+
+    def barrier():
+        if tdist:
+            tdist.barrier()
+
     for _ in range(args.warmup):
-        rd.spmm_local(a, b, c)
+        reset()
+        dm.run_multiply(f, A, B, Cm, **opts)
     torch.cuda.synchronize()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        ev[0].record(stream)
-        for i in range(args.steps):
-            rd.spmm_local(a, b, c)
-            ev[i + 1].record(stream)
-        torch.cuda.synchronize()
-        per = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
-        ms = ev[0].elapsed_time(ev[-1]) / args.steps
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ms = float(t.item())
-        # ---- e2e through the public API from pinned host buffers
-        rp, ci, vv = (x.cpu().pin_memory() for x in (a.row_ptr, a.col_idx, a.values))
-        bh = b.cpu().pin_memory()
-        ch = torch.empty_like(c, device="cpu").pin_memory()
-        h2d = sum(x.numel() * x.element_size() for x in (rp, ci, vv, bh))
-        d2h = ch.numel() * ch.element_size()
-        e2e_steps = max(1, min(args.steps, 5))
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(e2e_steps):
-            a.row_ptr.copy_(rp, non_blocking=True)
-            a.col_idx.copy_(ci, non_blocking=True)
-            a.values.copy_(vv, non_blocking=True)
-            b.copy_(bh, non_blocking=True)
-            c.zero_()
-            rd.spmm_local(a, b, c)
-            ch.copy_(c, non_blocking=True)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    L.rdmm_kernel_timing(1)
+    launches0 = L.rdmm_kernel_launches()
+    per, flops_local, steals = [], 0, 0
+    with ClockSampler(dev.index) as clk:
+        for _ in range(args.steps):
+            reset()
+            barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rep = dm.run_multiply(f, A, B, Cm, **opts)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            per.append(e0.elapsed_time(e1))
+            flops_local = rep.total_flops
+            steals += rep.total_steals
+    launches = L.rdmm_kernel_launches() - launches0
+    kind_id = 1 if cfg["kind"] == "spmm" else 2
+    kms, kcount = L.kernel_time(kind_id)
+    L.rdmm_kernel_timing(0)
+    ms_local = sum(per) / len(per)
+    if tdist:  # max over ranks of the device time; flops summed over ranks
+        t = torch.tensor([ms_local, float(flops_local), float(steals)], device=dev,
+                         dtype=torch.float64)
+        tmax = t[:1].clone()
+        tdist.all_reduce(tmax, op=tdist.ReduceOp.MAX)
+        tsum = t[1:].clone()
+        tdist.all_reduce(tsum, op=tdist.ReduceOp.SUM)
+        ms, total_flops, steals = float(tmax[0]), int(tsum[0]), int(tsum[1])
+    else:
+        ms, total_flops = ms_local, flops_local
+    out_nnz = Cm.nnz() if cfg["kind"] == "spgemm" else None
+
+    # ---- roofline of the dominant kernel on this rank (DESIGN.md §5)
     hbm, peak_src = peaks()
-    launch_ms = statistics.mean(per)
-    alg = spmm_bytes(m, k, n, nnz)
-    achieved = alg / (launch_ms * 1e-3) / 1e9
-    total_flops = flops * world
+    if cfg["kind"] == "spmm":
+        own_cols = min(tn, n)
+        ktiles = -(-k // tk)
+        # per-rank compulsory bytes: all A tiles once, own B and C columns once
+        alg = 4 * (m + 1) * ktiles + 8 * nnz_a + 4 * k * own_cols + 4 * m * own_cols
+        kernel = "spmm_stream+spmm_fixup (rdmm_spmm_csr), all launches of a step on this rank"
+    else:
+        alg = (2 * a_bytes + (m + 1) * 4 + 8 * (out_nnz or 0)) // world
+        kernel = "spgemm numeric tiers (rdmm_spgemm_numeric), per step on this rank"
+    kms_step = kms / max(1, args.steps)
+    achieved = alg / (kms_step * 1e-3) / 1e9 if kms_step > 0 else None
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": (achieved / hbm) if achieved else None,
+            "traffic": load_traffic(args.config, "spmm_stream" if kind_id == 1 else "spgemm",
+                                    world),
+            "algorithmic_bytes": alg, "peak_source": peak_src, "kernel": kernel,
+            "kernel_ms_per_step": kms_step, "kernel_launches_timed": kcount}
+
+    # ---- e2e: the same step through the public API from pinned host buffers
+    rp_h, ci_h, vv_h = (x.cpu().pin_memory() for x in (a.row_ptr, a.col_idx, a.values))
+    b_h = b.cpu().pin_memory() if b is not None else None
+    c_h = torch.empty((m, n), dtype=torch.float32).pin_memory() if cfg["kind"] == "spmm" else None
+    a_dev = rd.DeviceCsr(a.rows, a.cols, a.nnz, torch.empty_like(a.row_ptr),
+                         torch.empty_like(a.col_idx), torch.empty_like(a.values))
+    del a, b
+    e2e_steps = max(1, min(args.steps, 3))
+    h2d = d2h = 0
+    e2e_t = []
+    for _ in range(e2e_steps):
+        reset()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        a_dev.row_ptr.copy_(rp_h, non_blocking=True)
+        a_dev.col_idx.copy_(ci_h, non_blocking=True)
+        a_dev.values.copy_(vv_h, non_blocking=True)
+        torch.cuda.synchronize()
+        A.init_from_device(a_dev)
+        h2d = sum(x.numel() * x.element_size() for x in (rp_h, ci_h, vv_h))
+        if cfg["kind"] == "spmm":
+            B.init_from_device(b_h)  # pinned host -> this rank's B tiles
+            h2d += k * min(tn, n) * 4
+        else:
+            B.init_from_device(a_dev)
+        dm.run_multiply(f, A, B, Cm, **opts)
+        if cfg["kind"] == "spmm":
+            Cm.owned_to_host(c_h)
+            d2h = m * min(tn, n) * 4
+        else:
+            d2h = Cm.owned_to_host()
+        torch.cuda.synchronize()
+        barrier()
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_ms = 1e3 * sum(e2e_t) / len(e2e_t)
+    if tdist:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        e2e_ms = float(t[0])
+
     out = {
         "metric": METRIC,
         "value": total_flops / (ms * 1e-3) / 1e9,
@@ -237,27 +363,126 @@ def run_spmm_local(args, cfg, dev, rank, world):
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (reference generators, seeds A=1 B=2, built on device)",
-        "config": {"workload": args.config, "desc": cfg["desc"], "rows": m, "cols": k,
-                   "n": n, "nnz": nnz, "flop_per_step": flops,
-                   "path": "spmm_local (C-ABI rdmm_spmm_csr_f32), 1x1 grid",
-                   "l2": "inputs > L2 (B %.2f GB, C %.2f GB)" % (k * n * 4 / 1e9, m * n * 4 / 1e9)},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": load_traffic(args.config, "spmm_chunks"),
-                     "algorithmic_bytes": alg, "peak_source": peak_src,
-                     "kernel": "spmm_chunks+spmm_fixup (one spmm_local launch pair)",
-                     "launch_ms": launch_ms},
+        "config": {"workload": args.config, "desc": cfg["desc"], "rows": m, "cols": k, "n": n,
+                   "nnz": nnz_a, "flop_per_step": total_flops,
+                   "variant": variant, "grid": f"{pr}x{pc}", "tiles": [tm, tk, tn],
+                   "path": "run_multiply (host C-ABI rdmm_h_run_multiply) over the fabric",
+                   "l2": ("inputs > L2 (A %.2f GB, B and C %.2f GB each)"
+                          % (nnz_a * 8 / 1e9, m * n * 4 / 1e9)) if cfg["kind"] == "spmm"
+                   else "inputs + output > L2", "steals": steals},
+        "roofline": roof,
         "e2e": {"value": total_flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-        "gpu_launches": 2 * args.steps,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "timer": "host wall clock around upload + run_multiply + download"},
+        "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline_spmm(a, b, args.config)
+    if out_nnz is not None:
+        out["config"]["nnz_out"] = out_nnz
+    f.close()
     return out
+
+
+def run_summa_nccl(args, cfg, dev, rank, world):
+    """The comparison point: bulk-synchronous SUMMA with NCCL broadcasts of
+    A(i,k) along grid rows and B(k,j) along grid columns each phase, the
+    same sm_100a SpMM kernel, and a barrier per phase (algos.hpp:348-374
+    with the broadcast the reference emulates)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2311_18141_b200 as rd
+    from paper_2311_18141_b200.tile import extract_tile
+
+    assert cfg["kind"] == "spmm", "summa_nccl baseline is for SpMM configs"
+    a, b = gen_inputs(cfg, dev)
+    m, k, n = a.rows, a.cols, cfg["n"]
+    (pr, pc), (tm, tk, tn) = layout(cfg, world, args)
+    Mt, Kt, Nt = -(-m // tm), -(-k // tk), -(-n // tn)
+    gi, gj = rank // pc, rank % pc
+    rows_g = [dist.new_group([r * pc + c for c in range(pc)]) for r in range(pr)] \
+        if world > 1 else None
+    cols_g = [dist.new_group([r * pc + c for r in range(pr)]) for c in range(pc)] \
+        if world > 1 else None
+    my_row = [i for i in range(Mt) if i % pr == gi]
+    my_col = [j for j in range(Nt) if j % pc == gj]
+    dims = lambda i, kk: (i * tm, min(tm, m - i * tm), kk * tk, min(tk, k - kk * tk))  # noqa
+    A_own = {(i, kk): extract_tile(a, *dims(i, kk)) for i in range(Mt) for kk in range(Kt)
+             if i % pr == gi and kk % pc == gj}
+    B_own = {(kk, j): b[kk * tk:kk * tk + min(tk, k - kk * tk), j * tn:j * tn + min(tn, n - j * tn)]
+             .contiguous() for kk in range(Kt) for j in range(Nt)
+             if kk % pr == gi and j % pc == gj}
+    nnz_tile = {}
+    for i in range(Mt):
+        for kk in range(Kt):
+            t = extract_tile(a, *dims(i, kk))
+            nnz_tile[(i, kk)] = t.nnz
+            del t
+    C = {(i, j): torch.zeros((min(tm, m - i * tm), min(tn, n - j * tn)), device=dev)
+         for i in my_row for j in my_col}
+    flops_local = sum(2 * nnz_tile[(i, kk)] * min(tn, n - j * tn)
+                      for (i, j) in C for kk in range(Kt))
+    del a, b
+
+    def step():
+        for kk in range(Kt):
+            a_t, b_t = {}, {}
+            for i in my_row:
+                root = (i % pr) * pc + (kk % pc)
+                t = A_own.get((i, kk)) or rd.DeviceCsr.empty(
+                    min(tm, m - i * tm), min(tk, k - kk * tk), nnz_tile[(i, kk)], device=dev)
+                if world > 1 and pc > 1:
+                    dist.broadcast(t.row_ptr, root, group=rows_g[gi])
+                    if t.nnz:
+                        dist.broadcast(t.col_idx, root, group=rows_g[gi])
+                        dist.broadcast(t.values, root, group=rows_g[gi])
+                a_t[i] = t
+            for j in my_col:
+                root = (kk % pr) * pc + (j % pc)
+                t = B_own.get((kk, j))
+                if t is None:
+                    t = torch.empty((min(tk, k - kk * tk), min(tn, n - j * tn)), device=dev)
+                if world > 1 and pr > 1:
+                    dist.broadcast(t, root, group=cols_g[gj])
+                b_t[j] = t
+            for (i, j), c in C.items():
+                rd.spmm_local(a_t[i], b_t[j], c, c_zero=(kk == 0))
+            if world > 1:
+                dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    per = []
+    with ClockSampler(dev.index) as clk:
+        for _ in range(args.steps):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step()
+            e1.record()
+            torch.cuda.synchronize()
+            per.append(e0.elapsed_time(e1))
+    ms, total = sum(per) / len(per), flops_local
+    if world > 1:
+        tmax = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = torch.tensor([float(flops_local)], device=dev, dtype=torch.float64)
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms, total = float(tmax[0]), int(tsum[0])
+    return {"metric": METRIC, "value": total / (ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference generators, seeds A=1 B=2, built on device)",
+            "config": {"workload": args.config, "desc": cfg["desc"], "variant": "summa_nccl",
+                       "grid": f"{pr}x{pc}", "tiles": [tm, tk, tn],
+                       "path": "NCCL-broadcast SUMMA baseline (torch.distributed + rdmm SpMM)"},
+            "clocks": clk.summary()}
 
 
 # ----------------------------------------------------------- reference arm
@@ -267,6 +492,8 @@ def run_reference(args):
     """The reference's own CPU path (oracle/_ref: the unmodified reference
     headers) timed on this host with all its threads: run_multiply
     stationary_c over a ProcGrid as square as possible."""
+    import ctypes as C
+
     import numpy as np
 
     rank = int(os.environ.get("RANK", "0"))
@@ -280,56 +507,69 @@ def run_reference(args):
         return {"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}
     R, Pn = oracle.ref(), oracle.port()
     threads = int(R._hardware_concurrency()) or os.cpu_count() or 1
-    # grid as square as possible with pr*pc = threads
     pr = int(np.sqrt(threads))
     while threads % pr:
         pr -= 1
     pc = threads // pr
-    if cfg["kind"] != "spmm":
-        return {"impl": "reference", "unavailable": "reference arm implemented for SpMM configs"}
     a = Pn.rmat(cfg["scale"], cfg["ef"], seed=1) if cfg["gen"] == "rmat" else \
         Pn.uniform_tiles(1 << cfg["scale"], 1 << cfg["scale"], 1, cfg["d"], 1)
-    n = cfg["n"]
-    b = Pn.random_dense(a.cols, n, 2)
-    # bounded sample: every S-th row of A so one step is ~1-3 s on this host
-    S = 1 if a.nnz < 5_000_000 else 8
-    rp, nci, nvv = row_sample(a.row_ptr, a.col_idx, a.values, S)
-    hs = oracle.Csr(len(rp) - 1, a.cols, rp, nci, nvv)
-    m, k = hs.rows, hs.cols
-    tm, tk, tn = -(-m // pr), -(-k // pc), -(-n // pc)
-    ao, keep = oracle.as_orc(hs)
-    import ctypes as C
-
-    L = R.lib
-    L.ref_spmm_session_create.restype = C.c_void_p
-    L.ref_spmm_session_create.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64,
-                                          C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
-                                          C.POINTER(oracle.OrcCsr), C.c_void_p, C.c_uint64]
-    L.ref_spmm_session_run.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64,
-                                       C.POINTER(oracle.RefReport)]
-    L.ref_spmm_session_destroy.argtypes = [C.c_void_p]
-    sess = L.ref_spmm_session_create(pr, pc, m, k, n, tm, tk, tn, C.byref(ao), b.ctypes.data, 0)
-    if not sess:
-        return {"impl": "reference", "unavailable": "reference session setup failed"}
-    rep = oracle.RefReport()
-    times, flops = [], 0
-    for i in range(args.warmup + args.steps):
-        rc = L.ref_spmm_session_run(sess, oracle.VARIANTS["stationary_c"],
-                                    oracle.VARIANTS["stationary_a"], 0, C.byref(rep))
-        if rc:
-            return {"impl": "reference", "unavailable": f"run_multiply failed ({rc})"}
-        if i >= args.warmup:
-            times.append(rep.wall_seconds)
-            flops = rep.total_flops
-    L.ref_spmm_session_destroy(sess)
+    if cfg["kind"] == "spmm":
+        n = cfg["n"]
+        b = Pn.random_dense(a.cols, n, 2)
+        S = 1 if a.nnz < 5_000_000 else 8
+        rp, nci, nvv = row_sample(a.row_ptr, a.col_idx, a.values, S)
+        hs = oracle.Csr(len(rp) - 1, a.cols, rp, nci, nvv)
+        m, k = hs.rows, hs.cols
+        tm, tk, tn = -(-m // pr), -(-k // pc), -(-n // pc)
+        ao, keep = oracle.as_orc(hs)
+        L = R.lib
+        L.ref_spmm_session_create.restype = C.c_void_p
+        L.ref_spmm_session_create.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64,
+                                              C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                              C.POINTER(oracle.OrcCsr), C.c_void_p, C.c_uint64]
+        L.ref_spmm_session_run.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64,
+                                           C.POINTER(oracle.RefReport)]
+        L.ref_spmm_session_destroy.argtypes = [C.c_void_p]
+        sess = L.ref_spmm_session_create(pr, pc, m, k, n, tm, tk, tn, C.byref(ao),
+                                         b.ctypes.data, 0)
+        if not sess:
+            return {"impl": "reference", "unavailable": "reference session setup failed"}
+        rep = oracle.RefReport()
+        times, flops = [], 0
+        for i in range(args.warmup + args.steps):
+            rc = L.ref_spmm_session_run(sess, oracle.VARIANTS["stationary_c"],
+                                        oracle.VARIANTS["stationary_a"], 0, C.byref(rep))
+            if rc:
+                return {"impl": "reference", "unavailable": f"run_multiply failed ({rc})"}
+            if i >= args.warmup:
+                times.append(rep.wall_seconds)
+                flops = rep.total_flops
+        L.ref_spmm_session_destroy(sess)
+        sample = (f"run_multiply stationary_c, {pr}x{pc} ProcGrid, {threads} rank threads, "
+                  f"every {S}th row of A ({m} rows, {hs.nnz} nnz) x full B (N={n})")
+    else:
+        S = 64 if a.nnz < 2_000_000 else 1024
+        rp, nci, nvv = row_sample(a.row_ptr, a.col_idx, a.values, S)
+        hs = oracle.Csr(len(rp) - 1, a.cols, rp, nci, nvv)
+        c0 = oracle.Csr(hs.rows, a.cols, np.zeros(hs.rows + 1, np.uint32),
+                        np.zeros(0, np.uint32), np.zeros(0, np.float32))
+        times, flops = [], 0
+        for i in range(1 + args.steps):
+            _, rep = R.run_multiply_spgemm(hs, a, c0, variant="stationary_c", grid=(pr, pc),
+                                           tiles=(-(-hs.rows // pr), -(-a.cols // pc),
+                                                  -(-a.cols // pc)))
+            if i >= 1:
+                times.append(rep.max_total_seconds)
+                flops = rep.total_flops
+        sample = (f"run_multiply stationary_c SpGEMM, {pr}x{pc} ProcGrid, {threads} rank "
+                  f"threads, every {S}th row of A ({hs.rows} rows, {hs.nnz} nnz) x full A; "
+                  f"max per-rank algorithm time")
     sec = sum(times) / len(times)
     val = flops / sec / 1e9
-    sample = (f"run_multiply stationary_c, {pr}x{pc} ProcGrid, {threads} rank threads, "
-              f"every {S}th row of A ({m} rows, {hs.nnz} nnz) x full B (N={n})")
     return {
         "metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference generators, seeds A=1 B=2)",
         "config": {"workload": args.config, "desc": cfg["desc"], "sample": sample},
         "impl": "reference",
@@ -343,13 +583,23 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--variant", default=None,
+                    help="stationary_c | stationary_a | stationary_b | ws_random | "
+                         "ws_locality | summa_bsp | summa_nccl (baseline)")
+    ap.add_argument("--grid", default=None, help="RxC ProcGrid override")
+    ap.add_argument("--mtiles", type=int, default=0)
+    ap.add_argument("--ktiles", type=int, default=0)
+    ap.add_argument("--ntiles", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.variant is None:
+        args.variant = "stationary_c" if cfg["kind"] == "spmm" else "ws_locality"
 
     if args.impl == "reference":
         out = run_reference(args)
@@ -366,13 +616,17 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         torch.distributed.init_process_group("nccl", device_id=dev)
-    cfg = CONFIGS[args.config]
-    if cfg["kind"] != "spmm":
-        raise SystemExit("SpGEMM configs are not wired into bench.py yet")
-    out = run_spmm_local(args, cfg, dev, rank, world)
+    if args.variant == "summa_nccl":
+        out = run_summa_nccl(args, cfg, dev, rank, world)
+    else:
+        out = run_ours(args, cfg, dev, rank, world)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        a, b = gen_inputs(cfg, dev)
+        out["cpu_baseline"] = cpu_baseline(a, b, cfg)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
+        torch.distributed.barrier()
         torch.distributed.destroy_process_group()
 
 

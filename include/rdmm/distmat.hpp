@@ -135,7 +135,7 @@ class DistDense {  // distmat.hpp:92-205
       for (std::uint32_t j = 0; j < geom_.N; ++j) {
         if (owner(i, j) != ctx.rank()) continue;
         const std::uint32_t r = geom_.tile_rows(i), c = geom_.tile_cols(j);
-        GlobalPtr p = ctx.alloc(std::size_t(r) * c * sizeof(T));
+        GlobalPtr p = fresh_tile(ctx, i, j);
         if (fill) {
           DenseTile<T> t = fill(i, j);
           if (t.rows != r || t.cols != c) throw dimension_error("init fill produced wrong tile dims");
@@ -201,6 +201,31 @@ class DistDense {  // distmat.hpp:92-205
   GlobalPtr tile_ptr(std::uint32_t i, std::uint32_t j) const {
     return GlobalPtr::of(dir_[geom_.idx(i, j)]);
   }
+  // Collective: zero every owned tile in place (a fresh C for the next run).
+  void zero(RankCtx& ctx) {
+    for (std::uint32_t i = 0; i < geom_.M; ++i)
+      for (std::uint32_t j = 0; j < geom_.N; ++j) {
+        if (owner(i, j) != ctx.rank()) continue;
+        GlobalPtr p = tile_ptr(i, j);
+        check(rdmm_memset(fabric_->raw(p, ctx.rank()), 0, p.length, ctx.stream(0)), "zero");
+        zero_[geom_.idx(i, j)] = 1;
+      }
+    ctx.barrier();
+  }
+  // Copy the caller's owned tiles into a row-major global host array (the
+  // device->host half of an end-to-end call; other ranks' tiles untouched).
+  void owned_to_host(RankCtx& ctx, T* global, std::uint64_t ld) {
+    for (std::uint32_t i = 0; i < geom_.M; ++i)
+      for (std::uint32_t j = 0; j < geom_.N; ++j) {
+        if (owner(i, j) != ctx.rank()) continue;
+        const std::uint32_t r = geom_.tile_rows(i), c = geom_.tile_cols(j);
+        T* dst = global + std::uint64_t(i) * geom_.tm * ld + std::uint64_t(j) * geom_.tn;
+        check(rdmm_memcpy2d(dst, ld * sizeof(T), fabric_->raw(tile_ptr(i, j), ctx.rank()),
+                            c * sizeof(T), c * sizeof(T), r, ctx.stream(0)),
+              "owned_to_host");
+      }
+    check(rdmm_stream_sync(ctx.stream(0)), "owned_to_host");
+  }
   // B200: zero-tracking so the first product into a fresh tile skips reading C.
   bool tile_is_zero(std::uint32_t i, std::uint32_t j) const { return zero_[geom_.idx(i, j)]; }
   void mark_nonzero(std::uint32_t i, std::uint32_t j) { zero_[geom_.idx(i, j)] = 0; }
@@ -223,12 +248,18 @@ class DistDense {  // distmat.hpp:92-205
   }
 
  private:
+  // Re-initialisation reuses the tile's allocation (same geometry).
+  GlobalPtr fresh_tile(RankCtx& ctx, std::uint32_t i, std::uint32_t j) {
+    const rdmm_gptr old = dir_[geom_.idx(i, j)];
+    if (old.length) return GlobalPtr::of(old);
+    return ctx.alloc(std::size_t(geom_.tile_rows(i)) * geom_.tile_cols(j) * sizeof(T));
+  }
   void init_from_any(RankCtx& ctx, const T* global, std::uint64_t ld) {
     for (std::uint32_t i = 0; i < geom_.M; ++i)
       for (std::uint32_t j = 0; j < geom_.N; ++j) {
         if (owner(i, j) != ctx.rank()) continue;
         const std::uint32_t r = geom_.tile_rows(i), c = geom_.tile_cols(j);
-        GlobalPtr p = ctx.alloc(std::size_t(r) * c * sizeof(T));
+        GlobalPtr p = fresh_tile(ctx, i, j);
         const T* src = global + std::uint64_t(i) * geom_.tm * ld + std::uint64_t(j) * geom_.tn;
         check(rdmm_memcpy2d(fabric_->raw(p, ctx.rank()), c * sizeof(T), src, ld * sizeof(T),
                             c * sizeof(T), r, ctx.stream(0)),
@@ -290,6 +321,7 @@ class DistSparse {  // distmat.hpp:210-398
         CsrTile<T> t = fill ? fill(i, j) : CsrTile<T>(geom_.tile_rows(i), geom_.tile_cols(j));
         if (t.rows != geom_.tile_rows(i) || t.cols != geom_.tile_cols(j))
           throw dimension_error("init fill produced wrong tile dims");
+        drop_tile(ctx, i, j);
         dir_[geom_.idx(i, j)] = store_host(ctx, t);
       }
     ctx.barrier();
@@ -308,6 +340,7 @@ class DistSparse {  // distmat.hpp:210-398
       for (std::uint32_t j = 0; j < geom_.N; ++j) {
         if (owner(i, j) != ctx.rank()) continue;
         const std::uint32_t r = geom_.tile_rows(i), c = geom_.tile_cols(j);
+        drop_tile(ctx, i, j);
         Entry e;
         e.row_ptr = ctx.alloc((std::uint64_t(r) + 1) * sizeof(index_t)).c();
         auto* rp = static_cast<index_t*>(fabric_->raw(GlobalPtr::of(e.row_ptr), ctx.rank()));
@@ -417,6 +450,28 @@ class DistSparse {  // distmat.hpp:210-398
     ctx.barrier();
   }
 
+  // Bytes of the caller's owned tiles copied to host buffers (the
+  // device->host half of an end-to-end call); returns the bytes moved.
+  std::uint64_t owned_to_host(RankCtx& ctx, std::vector<char>& out) {
+    std::uint64_t bytes = 0;
+    for (std::uint32_t i = 0; i < geom_.M; ++i)
+      for (std::uint32_t j = 0; j < geom_.N; ++j) {
+        if (owner(i, j) != ctx.rank()) continue;
+        const Entry& e = dir_[geom_.idx(i, j)];
+        for (auto g : {e.row_ptr, e.col_idx, e.values}) {
+          const std::size_t o = out.size();
+          out.resize(o + g.length);
+          if (g.length)
+            check(rdmm_memcpy(out.data() + o, fabric_->raw(GlobalPtr::of(g), ctx.rank()), g.length,
+                              ctx.stream(0)),
+                  "owned_to_host");
+          bytes += g.length;
+        }
+      }
+    check(rdmm_stream_sync(ctx.stream(0)), "owned_to_host");
+    return bytes;
+  }
+
   // Host-side gather; bypasses traffic (distmat.hpp:359-377).
   CsrTile<T> to_global() const {
     CsrTile<T> g(static_cast<index_t>(geom_.m), static_cast<index_t>(geom_.n));
@@ -464,6 +519,15 @@ class DistSparse {  // distmat.hpp:210-398
     v.col_idx = static_cast<const index_t*>(fabric_->raw(GlobalPtr::of(e.col_idx), viewer));
     v.values = static_cast<const T*>(fabric_->raw(GlobalPtr::of(e.values), viewer));
     return v;
+  }
+  // Re-initialisation releases the tile's previous allocations.
+  void drop_tile(RankCtx& ctx, std::uint32_t i, std::uint32_t j) {
+    Entry& e = dir_[geom_.idx(i, j)];
+    if (!e.row_ptr.length) return;
+    ctx.free(GlobalPtr::of(e.values));
+    ctx.free(GlobalPtr::of(e.row_ptr));
+    ctx.free(GlobalPtr::of(e.col_idx));
+    e = Entry{};
   }
   void check_replace(RankCtx& ctx, std::uint32_t i, std::uint32_t j, index_t rows, index_t cols) {
     geom_.check(i, j);

@@ -51,6 +51,14 @@ typedef enum {
 const char* rdmm_last_error(void);
 /* Library version string and the compiled device architecture. */
 const char* rdmm_version(void);
+/* Number of this library's kernels launched so far (process-wide). */
+unsigned long long rdmm_kernel_launches(void);
+/* Device timing of the hot kernels: when enabled, CUDA events are recorded
+ * on the launching stream around each launch (kind 1 = SpMM launch pair,
+ * 2 = SpGEMM numeric, 3 = dense accumulate).  _get sums the durations of
+ * one kind (-1: all) recorded since the last rdmm_kernel_timing() call. */
+void rdmm_kernel_timing(int enable);
+int rdmm_kernel_timing_get(int kind, double* total_ms, unsigned long long* count);
 
 /* ------------------------------------------------------------------ SpMM */
 /*

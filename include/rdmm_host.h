@@ -51,6 +51,16 @@ int rdmm_h_sparse_init(rdmm_h_matrix* mat, const uint32_t* row_ptr,
                        uint64_t nnz, int on_device);
 int rdmm_h_dense_init(rdmm_h_matrix* mat, const void* global, uint64_t ld);
 
+/* Collective: zero every tile of a dense matrix in place (fresh C). */
+int rdmm_h_dense_zero(rdmm_h_matrix* mat);
+/* End-to-end download: each local rank copies ITS tiles of the result into
+ * the host array (dense: row-major global layout; sparse: the raw CSR arrays
+ * of its tiles, concatenated, *bytes set to the amount moved). */
+int rdmm_h_dense_owned_to_host(rdmm_h_matrix* mat, void* global, uint64_t ld);
+int rdmm_h_sparse_owned_to_host(rdmm_h_matrix* mat, uint64_t* bytes);
+/* The compute stream of a local rank (timing events go there). */
+void* rdmm_h_fabric_stream(rdmm_h_fabric* f, uint32_t rank);
+
 /* Host gathers (verification; bypass traffic accounting). */
 int rdmm_h_dense_to_host(rdmm_h_matrix* mat, void* out);
 int rdmm_h_sparse_nnz(rdmm_h_matrix* mat, uint64_t* nnz);

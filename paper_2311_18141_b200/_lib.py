@@ -75,6 +75,13 @@ def _fn(name, args, res=cint):
 
 rdmm_last_error = _fn("rdmm_last_error", [], C.c_char_p)
 rdmm_version = _fn("rdmm_version", [], C.c_char_p)
+rdmm_kernel_launches = _fn("rdmm_kernel_launches", [], C.c_ulonglong)
+rdmm_kernel_timing = _fn("rdmm_kernel_timing", [cint], None)
+rdmm_kernel_timing_get = _fn("rdmm_kernel_timing_get", [cint, P(C.c_double), P(C.c_ulonglong)])
+rdmm_csr_extract_count = _fn("rdmm_csr_extract_count", [vp, vp, u64, u32, u64, u32, vp, P(u64),
+                                                        vp])
+rdmm_csr_extract_fill = _fn("rdmm_csr_extract_fill", [cint, vp, vp, vp, u64, u32, u64, u32, vp,
+                                                      vp, vp, vp])
 rdmm_spmm_workspace_bytes = _fn("rdmm_spmm_workspace_bytes", [u32, u64, u32, cint], sz)
 _spmm_args = [u32, u32, u32, u64, vp, vp, vp, vp, u64, vp, u64, vp, sz, vp, P(u64)]
 rdmm_spmm_csr_f32 = _fn("rdmm_spmm_csr_f32", _spmm_args)
@@ -115,6 +122,13 @@ def check(rc: int, what: str = "") -> None:
     msg = (rdmm_last_error() or b"").decode(errors="replace")
     cls = _ERRORS.get(rc, RdmmError)
     raise cls(f"{what}: {msg}" if what else msg)
+
+
+def kernel_time(kind: int = -1):
+    """(total ms, launches) of timed kernels since kernel_timing(True)."""
+    ms, n = C.c_double(0), C.c_ulonglong(0)
+    rdmm_kernel_timing_get(kind, C.byref(ms), C.byref(n))
+    return ms.value, n.value
 
 
 def loaded_path() -> str:

@@ -43,6 +43,19 @@ inline int num_sms() {
 // their kernels on one stream per device (the algorithms in this library do).
 void* scratch(size_t bytes, int slot = 0);
 
+// Launch accounting for bench.py's gpu_launches claim (our kernels only).
+void count_launch(unsigned n = 1);
+
+// Optional device timing of the hot kernels (CUDA events on the launching
+// stream around each launch; rdmm_kernel_timing_* in the C-ABI).
+struct KernelTimer {
+  cudaEvent_t start = nullptr;
+  cudaStream_t stream = nullptr;
+  int kind = 0;
+  KernelTimer(cudaStream_t s, int kind);
+  ~KernelTimer();
+};
+
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) {
   return (a + b - 1) / b;
 }

@@ -41,6 +41,8 @@ int dense_add(uint32_t rows, uint32_t cols, T* c, uint64_t ldc, const T* x,
   const int blocks =
       int(std::min<uint64_t>(uint64_t(num_sms()) * 8, ceil_div(units, 256)));
   cudaStream_t s = as_stream(stream);
+  KernelTimer timer(s, 3);
+  count_launch();
   if (vec)
     dense_add_vec<T, V><<<blocks, 256, 0, s>>>(
         rows, cols / L, reinterpret_cast<V*>(c), ldc / L,

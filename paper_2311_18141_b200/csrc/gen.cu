@@ -192,6 +192,7 @@ struct rdmm_gen_state {
 
 extern "C" int rdmm_gen_rng_at(uint64_t seed, uint64_t first, uint64_t count,
                                uint64_t* out, rdmm_stream_t stream) {
+  count_launch();
   if (!count) return RDMM_OK;
   k_rng_at<<<grid_for(count), 256, 0, as_stream(stream)>>>(seed, first, count,
                                                            out);
@@ -204,6 +205,7 @@ extern "C" int rdmm_gen_random_dense(uint64_t count, uint64_t seed,
                                      rdmm_stream_t stream) {
   if (!count) return RDMM_OK;
   const uint64_t mod = uint64_t(max_value + 1);
+  count_launch();
   if (dtype_bytes == 8)
     k_random_dense<double><<<grid_for(count), 256, 0, as_stream(stream)>>>(
         count, seed, mod, static_cast<double*>(out));
@@ -218,6 +220,7 @@ extern "C" int rdmm_gen_real_twin(uint64_t count, uint64_t seed,
                                   int dtype_bytes, void* out,
                                   rdmm_stream_t stream) {
   if (!count) return RDMM_OK;
+  count_launch();
   if (dtype_bytes == 8)
     k_real_twin<double><<<grid_for(count), 256, 0, as_stream(stream)>>>(
         count, seed, static_cast<double*>(out));
@@ -286,6 +289,7 @@ extern "C" int rdmm_gen_rmat_begin(double a, double b, double c, double d,
     return fail(RDMM_ERR_CUDA, "rmat: out of device memory");
   }
   if (edges) {
+    count_launch();
     k_rmat_edges<<<grid_for(edges), 256>>>(edges, scale, seed, a, a + b,
                                            a + b + c, keys.as<uint64_t>());
     int rc = sort_unique(st, keys, edges, std::max(1, int(2 * scale)));
@@ -345,8 +349,10 @@ extern "C" int rdmm_gen_uniform_tiles_begin(uint64_t m, uint64_t k, uint32_t p,
           delete st;
           return fail(RDMM_ERR_CUDA, "uniform_tiles: out of device memory");
         }
+        count_launch();
         k_draws<<<grid_for(D), 256>>>(D, seed, ctr, area, cell.as<uint64_t>(),
                                       idx.as<uint32_t>());
+        count_launch();
         k_unsorted_cells<<<grid_for(D), 256>>>(D, seed, ctr, area,
                                                cell_u.as<uint64_t>());
         size_t tb = 0, tb2 = 0;
@@ -365,6 +371,7 @@ extern "C" int rdmm_gen_uniform_tiles_begin(uint64_t m, uint64_t k, uint32_t p,
                                         idx_s.as<uint32_t>(), int64_t(D), 0,
                                         bits_for(area - 1 ? area - 1 : 1));
         cudaMemset(flag.p, 0, D * 4);
+        count_launch();
         k_first_occ<<<grid_for(D), 256>>>(cell_s.as<uint64_t>(),
                                           idx_s.as<uint32_t>(), D,
                                           flag.as<uint32_t>());
@@ -372,6 +379,7 @@ extern "C" int rdmm_gen_uniform_tiles_begin(uint64_t m, uint64_t k, uint32_t p,
                                       cnt.as<uint32_t>(), int64_t(D));
         unsigned long long T = 0;
         cudaMemset(Tbuf.p, 0, 8);
+        count_launch();
         k_find_T<<<grid_for(D), 256>>>(cnt.as<uint32_t>(), D, per_tile,
                                        static_cast<unsigned long long*>(Tbuf.p));
         if (cudaMemcpy(&T, Tbuf.p, 8, cudaMemcpyDeviceToHost) != cudaSuccess)
@@ -384,6 +392,7 @@ extern "C" int rdmm_gen_uniform_tiles_begin(uint64_t m, uint64_t k, uint32_t p,
           D *= 2;
           continue;
         }
+        count_launch();
         k_emit_cells<<<grid_for(T), 256>>>(
             cell_u.as<uint64_t>(), flag.as<uint32_t>(), cnt.as<uint32_t>(), T,
             tk, uint64_t(ti) * tm, uint64_t(tj) * tk, k,
@@ -411,10 +420,12 @@ extern "C" int rdmm_gen_finish(rdmm_gen_state* st, int dtype_bytes,
                                void* values) {
   if (!st) return fail(RDMM_ERR_INVALID, "gen_finish: null state");
   const uint64_t rows = st->rows, nnz = st->nnz;
+  count_launch();
   k_row_ptr<<<grid_for(rows + 1), 256>>>(st->keys.as<uint64_t>(), nnz, rows,
                                          st->cols, row_ptr);
   const uint32_t* counts = st->multiplicity ? st->counts.as<uint32_t>() : nullptr;
   if (nnz) {
+    count_launch();
     if (dtype_bytes == 8)
       k_cols_vals<double><<<grid_for(nnz), 256>>>(
           st->keys.as<uint64_t>(), counts, nnz, st->cols, col_idx,

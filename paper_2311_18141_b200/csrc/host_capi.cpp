@@ -1,5 +1,6 @@
 // host_capi.cpp -- C-ABI over the C++ driver layer (include/rdmm/*.hpp),
 // see include/rdmm_host.h.
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -283,3 +284,53 @@ extern "C" int rdmm_h_run_multiply(rdmm_h_fabric* f, rdmm_h_matrix* A, rdmm_h_ma
 }
 
 extern "C" void rdmm_h_free(void* p) { std::free(p); }
+
+extern "C" int rdmm_h_dense_zero(rdmm_h_matrix* mat) {
+  return guarded([&] {
+    if (mat->kind != 1) throw std::invalid_argument("not a dense matrix");
+    if (mat->dtype == 8) {
+      auto& m = *std::get<std::unique_ptr<DistDense<double>>>(mat->m);
+      run_ranks(*mat->fab->f, [&](RankCtx& ctx) { m.zero(ctx); });
+    } else {
+      auto& m = *std::get<std::unique_ptr<DistDense<float>>>(mat->m);
+      run_ranks(*mat->fab->f, [&](RankCtx& ctx) { m.zero(ctx); });
+    }
+  });
+}
+
+extern "C" int rdmm_h_dense_owned_to_host(rdmm_h_matrix* mat, void* global, uint64_t ld) {
+  return guarded([&] {
+    if (mat->kind != 1) throw std::invalid_argument("not a dense matrix");
+    if (mat->dtype == 8) {
+      auto& m = *std::get<std::unique_ptr<DistDense<double>>>(mat->m);
+      run_ranks(*mat->fab->f,
+                [&](RankCtx& ctx) { m.owned_to_host(ctx, static_cast<double*>(global), ld); });
+    } else {
+      auto& m = *std::get<std::unique_ptr<DistDense<float>>>(mat->m);
+      run_ranks(*mat->fab->f,
+                [&](RankCtx& ctx) { m.owned_to_host(ctx, static_cast<float*>(global), ld); });
+    }
+  });
+}
+
+extern "C" int rdmm_h_sparse_owned_to_host(rdmm_h_matrix* mat, uint64_t* bytes) {
+  return guarded([&] {
+    if (mat->kind != 0) throw std::invalid_argument("not a sparse matrix");
+    std::atomic<uint64_t> total{0};
+    auto go = [&](auto& m) {
+      run_ranks(*mat->fab->f, [&](RankCtx& ctx) {
+        std::vector<char> buf;
+        total += m.owned_to_host(ctx, buf);
+      });
+    };
+    if (mat->dtype == 8)
+      go(*std::get<std::unique_ptr<DistSparse<double>>>(mat->m));
+    else
+      go(*std::get<std::unique_ptr<DistSparse<float>>>(mat->m));
+    *bytes = total;
+  });
+}
+
+extern "C" void* rdmm_h_fabric_stream(rdmm_h_fabric* f, uint32_t rank) {
+  return rdmm_fabric_stream(f->f->handle(), rank, 0);
+}

@@ -475,6 +475,7 @@ int launch_sym_hash(const uint32_t* list, uint32_t count,
   const int threads = G == 32 ? 256 : G;
   const uint64_t blocks = std::min<uint64_t>(ceil_div(count, RPB),
                                              uint64_t(num_sms()) * 64);
+  count_launch();
   fn<<<unsigned(blocks), threads, sm, s>>>(list, count, terms, nterms, cnt64);
   return 0;
 }
@@ -493,6 +494,7 @@ int launch_num_hash(const uint32_t* list, uint32_t count,
   const int threads = G == 32 ? 256 : G;
   const uint64_t blocks = std::min<uint64_t>(ceil_div(count, RPB),
                                              uint64_t(num_sms()) * 64);
+  count_launch();
   fn<<<unsigned(blocks), threads, sm, s>>>(list, count, terms, nterms, crp,
                                            cci, cv, ident);
   return 0;
@@ -561,6 +563,7 @@ int symbolic_impl(uint32_t rows, uint32_t ncols, const rdmm_spgemm_term* terms,
   if (rows && nterms) {
     const unsigned blocks = unsigned(std::min<uint64_t>(
         ceil_div(rows, 8), uint64_t(num_sms()) * 16));
+    count_launch();
     k_bin_sym<T><<<blocks, 256, 8 * size_t(nterms), s>>>(rows, td, nterms, lists,
                                                          tc, tub, cnt);
     RDMM_CUDA_TRY(cudaGetLastError());
@@ -591,6 +594,7 @@ int symbolic_impl(uint32_t rows, uint32_t ncols, const rdmm_spgemm_term* terms,
     const uint32_t blocks = std::min<uint32_t>(hc[5], uint32_t(num_sms()));
     RDMM_CUDA_TRY(P->bitmaps.ensure(size_t(blocks) * nwords * 4));
     RDMM_CUDA_TRY(cudaMemsetAsync(P->bitmaps.p, 0, size_t(blocks) * nwords * 4, s));
+    count_launch();
     k_sym_dense<T><<<blocks, kDenseThreads, 0, s>>>(
         L(5), hc[5], td, nterms, cnt, P->bitmaps.as<uint32_t>(), nwords);
   }
@@ -609,11 +613,13 @@ int symbolic_impl(uint32_t rows, uint32_t ncols, const rdmm_spgemm_term* terms,
   if (rows) {
     const unsigned nb = unsigned(std::min<uint64_t>(ceil_div(rows + 1, 256),
                                                     uint64_t(num_sms()) * 8));
+    count_launch();
     k_bin_num<<<nb, 256, 0, s>>>(rows, cnt, lists, tc + kTiers);
   }
   if (c_row_ptr) {
     const unsigned nb = unsigned(std::min<uint64_t>(ceil_div(rows + 1, 256),
                                                     uint64_t(num_sms()) * 8));
+    count_launch();
     k_rowptr32<<<nb, 256, 0, s>>>(P->pre64.as<uint64_t>(), rows + 1, c_row_ptr);
   }
   RDMM_CUDA_TRY(cudaMemcpyAsync(hc, tc, sizeof(uint32_t) * 2 * kTiers,
@@ -643,6 +649,7 @@ int numeric_impl(rdmm_spgemm_plan* P, uint32_t* cci, T* cv, cudaStream_t s) {
   // -0.0 is the exact additive identity (keeps signed zeros of csr_add);
   // products start from +0.0 like the reference accumulator (tile.hpp:232).
   const T ident = P->ident_only ? T(-0.0) : T(0);
+  KernelTimer timer(s, 2);
   const uint32_t* crp = P->c_row_ptr;
   const uint32_t* c = P->num_count;
   int rc = 0;
@@ -659,8 +666,10 @@ int numeric_impl(rdmm_spgemm_plan* P, uint32_t* cci, T* cv, cudaStream_t s) {
     RDMM_CUDA_TRY(cudaMemsetAsync(P->bitmaps.p, 0, size_t(blocks) * nwords * 4, s));
     RDMM_CUDA_TRY(P->dense.ensure(size_t(blocks) * P->ncols * sizeof(T)));
     const size_t nd = size_t(blocks) * P->ncols;
+    count_launch();
     k_fill<T><<<unsigned(std::min<uint64_t>(ceil_div(nd, 256), 4096)), 256, 0, s>>>(
         P->dense.as<T>(), nd, ident);
+    count_launch();
     k_num_dense<T><<<blocks, kDenseThreads, 0, s>>>(
         L(5), c[5], td, nt, crp, cci, cv, P->bitmaps.as<uint32_t>(),
         P->dense.as<T>(), nwords, P->ncols, ident);

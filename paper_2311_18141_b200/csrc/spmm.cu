@@ -640,7 +640,9 @@ int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
   a.tail_val = reinterpret_cast<T*>(base + vbytes);
   a.tail_row = reinterpret_cast<int32_t*>(base + 2 * vbytes);
   const uint32_t nvec_total = n / P.VEC;
+  KernelTimer timer(s, 1);
   for (uint32_t v0 = 0; v0 < nvec_total; v0 += P.pv) {
+    count_launch(2);
     const uint32_t nv = std::min<uint32_t>(P.pv, nvec_total - v0);
     int nvp = 1;
     const int g = groups_for(nv, &nvp);

@@ -95,6 +95,7 @@ extern "C" int rdmm_csr_extract_count(const uint32_t* rp, const uint32_t* ci,
   if (!cnt) return fail(RDMM_ERR_CUDA, "extract: scratch allocation failed");
   const unsigned blocks = unsigned(std::max<uint64_t>(
       1, std::min<uint64_t>(ceil_div(nrows, 256), uint64_t(num_sms()) * 8)));
+  count_launch();
   k_extract_count<<<blocks, 256, 0, s>>>(rp, ci, r0, nrows, c0, c0 + ncols,
                                          static_cast<uint32_t*>(cnt));
   size_t tb = 0;
@@ -120,6 +121,7 @@ extern "C" int rdmm_csr_extract_fill(int dtype_bytes, const uint32_t* rp,
   cudaStream_t s = as_stream(stream);
   const unsigned blocks = unsigned(std::max<uint64_t>(
       1, std::min<uint64_t>(ceil_div(nrows, 8), uint64_t(num_sms()) * 16)));
+  count_launch();
   if (dtype_bytes == 8)
     k_extract_fill<double><<<blocks, 256, 0, s>>>(
         rp, ci, static_cast<const double*>(val), r0, nrows, c0, c0 + ncols,
@@ -143,6 +145,7 @@ extern "C" int rdmm_tile_sum(int dtype_bytes, uint32_t rows, uint32_t cols,
   if (total) {
     const unsigned blocks = unsigned(std::max<uint64_t>(
         1, std::min<uint64_t>(ceil_div(total, 256), uint64_t(num_sms()) * 4)));
+    count_launch();
     if (dtype_bytes == 8)
       k_tile_sum<double><<<blocks, 256, 0, s>>>(rows, cols, ld,
                                                 static_cast<const double*>(p), d);
@@ -156,6 +159,7 @@ extern "C" int rdmm_tile_sum(int dtype_bytes, uint32_t rows, uint32_t cols,
 }
 
 extern "C" int rdmm_spin_delay(uint64_t ns, rdmm_stream_t stream) {
+  count_launch();
   if (!ns) return RDMM_OK;
   k_spin<<<1, 1, 0, as_stream(stream)>>>(ns);
   RDMM_CUDA_TRY(cudaGetLastError());

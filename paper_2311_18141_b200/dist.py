@@ -57,6 +57,14 @@ _h.rdmm_h_dense_to_host.argtypes = [_vp, _vp]
 _h.rdmm_h_sparse_nnz.argtypes = [_vp, C.POINTER(_u64)]
 _h.rdmm_h_sparse_to_host.argtypes = [_vp, _vp, _vp, _vp]
 _h.rdmm_h_run_multiply.argtypes = [_vp, _vp, _vp, _vp, C.POINTER(Options), C.POINTER(Report)]
+_h.rdmm_h_dense_zero.argtypes = [_vp]
+_h.rdmm_h_dense_zero.restype = _int
+_h.rdmm_h_dense_owned_to_host.argtypes = [_vp, _vp, _u64]
+_h.rdmm_h_dense_owned_to_host.restype = _int
+_h.rdmm_h_sparse_owned_to_host.argtypes = [_vp, C.POINTER(_u64)]
+_h.rdmm_h_sparse_owned_to_host.restype = _int
+_h.rdmm_h_fabric_stream.argtypes = [_vp, _u32]
+_h.rdmm_h_fabric_stream.restype = _vp
 _h.rdmm_h_free.argtypes = [_vp]
 _h.rdmm_h_free.restype = None
 _h.rdmm_tile_fetches.argtypes = [_vp, _vp, _u64]
@@ -108,6 +116,10 @@ class Fabric:
     @property
     def handle(self):
         return _h.rdmm_h_fabric_handle(self._h)
+
+    def stream(self, rank):
+        """cudaStream_t (int) of a local rank's compute stream."""
+        return _h.rdmm_h_fabric_stream(self._h, rank)
 
     def tile_fetches(self):
         n = _h.rdmm_tile_fetches(self.handle, None, 0)
@@ -187,6 +199,12 @@ class DistSparse(_Mat):
                                       dcsr.values.data_ptr() if dcsr.nnz else None, dcsr.nnz, 1),
                 "init_from_device")
 
+    def owned_to_host(self):
+        """D2H of this process's tiles (raw CSR arrays); returns bytes."""
+        n = C.c_uint64(0)
+        L.check(_h.rdmm_h_sparse_owned_to_host(self._h, C.byref(n)), "owned_to_host")
+        return n.value
+
     def nnz(self):
         n = C.c_uint64(0)
         L.check(_h.rdmm_h_sparse_nnz(self._h, C.byref(n)), "nnz")
@@ -216,10 +234,20 @@ class DistDense(_Mat):
         L.check(_h.rdmm_h_dense_init(self._h, g.ctypes.data, self.n), "init_from_global")
 
     def init_from_device(self, tensor):
-        """B200: scatter from a device (or pinned host) tensor, row-major."""
+        """B200: scatter from a device (or pinned host) tensor, row-major;
+        re-initialisation reuses the tiles in place."""
         assert tuple(tensor.shape) == (self.m, self.n) and tensor.stride(1) == 1
         L.check(_h.rdmm_h_dense_init(self._h, tensor.data_ptr(), tensor.stride(0)),
                 "init_from_device")
+
+    def zero(self):
+        L.check(_h.rdmm_h_dense_zero(self._h), "zero")
+
+    def owned_to_host(self, out):
+        """D2H of this process's tiles into `out` (m x n row-major, e.g. a
+        pinned tensor or numpy array); returns bytes moved."""
+        ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+        L.check(_h.rdmm_h_dense_owned_to_host(self._h, ptr, self.n), "owned_to_host")
 
     def to_global(self):
         out = np.zeros((self.m, self.n), self.dtype)

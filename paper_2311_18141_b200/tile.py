@@ -167,6 +167,25 @@ def csr_add(a: DeviceCsr, b: DeviceCsr, stream=None) -> DeviceCsr:
                         device=a.device, stream=stream)[0]
 
 
+def extract_tile(g: DeviceCsr, r0: int, nrows: int, c0: int, ncols: int,
+                 stream=None) -> DeviceCsr:
+    """Tile (r0.., c0..) of a device CSR, columns rebased (distmat.hpp:265-282)."""
+    out = DeviceCsr.empty(nrows, ncols, 0, dtype=g.dtype, device=g.device)
+    nnz = C.c_uint64(0)
+    L.check(L.rdmm_csr_extract_count(g.row_ptr.data_ptr(), g.col_idx.data_ptr(), r0, nrows, c0,
+                                     ncols, out.row_ptr.data_ptr(), C.byref(nnz),
+                                     _stream(stream)), "extract")
+    n = nnz.value
+    out.nnz = n
+    out.col_idx = torch.empty(max(n, 1), dtype=torch.int32, device=g.device)[:n]
+    out.values = torch.empty(max(n, 1), dtype=g.dtype, device=g.device)[:n]
+    L.check(L.rdmm_csr_extract_fill(_wcode(g.dtype), g.row_ptr.data_ptr(), g.col_idx.data_ptr(),
+                                    g.values.data_ptr(), r0, nrows, c0, ncols,
+                                    out.row_ptr.data_ptr(), out.col_idx.data_ptr(),
+                                    out.values.data_ptr(), _stream(stream)), "extract")
+    return out
+
+
 def dense_add_into(c: torch.Tensor, x: torch.Tensor, stream=None) -> None:
     """c += x (tile.hpp:300-307)."""
     if c.shape != x.shape:
