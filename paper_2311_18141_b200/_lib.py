@@ -115,6 +115,32 @@ rdmm_gen_finish = _fn("rdmm_gen_finish", [vp, cint, vp, vp, vp])
 rdmm_gen_abort = _fn("rdmm_gen_abort", [vp], None)
 
 
+# ---- fabric (control plane + heaps), include/rdmm_cuda.h
+
+
+class Gptr(C.Structure):
+    _fields_ = [("rank", u32), ("pad_", u32), ("offset", u64), ("length", u64)]
+
+
+class FabricConfig(C.Structure):
+    _fields_ = [("nranks", u32), ("node_group", u32), ("heap_bytes", u64),
+                ("queue_capacity", u64), ("ctrl_bytes", u64), ("first_local", u32),
+                ("nlocal", u32), ("devices", P(cint)), ("session", C.c_char_p)]
+
+
+rdmm_fabric_create = _fn("rdmm_fabric_create", [P(FabricConfig), P(vp)])
+rdmm_fabric_destroy = _fn("rdmm_fabric_destroy", [vp], None)
+rdmm_ctrl_cells = _fn("rdmm_ctrl_cells", [vp, u32, u64, u64, P(Gptr)])
+rdmm_ctrl_release = _fn("rdmm_ctrl_release", [vp, u32, u64])
+rdmm_ctrl_host = _fn("rdmm_ctrl_host", [vp, Gptr], vp)
+rdmm_fetch_add_i64 = _fn("rdmm_fetch_add_i64", [vp, u32, Gptr, i64, P(i64)])
+rdmm_queue_open = _fn("rdmm_queue_open", [vp, u32, u64, u64, P(u64)])
+rdmm_queue_push = _fn("rdmm_queue_push", [vp, u32, u64, Gptr, vp, u32])
+rdmm_queue_pop = _fn("rdmm_queue_pop", [vp, u32, u64, P(Gptr), vp, u32, P(cint)])
+rdmm_barrier = _fn("rdmm_barrier", [vp, u32])
+rdmm_fabric_abort = _fn("rdmm_fabric_abort", [vp, C.c_char_p], None)
+
+
 def check(rc: int, what: str = "") -> None:
     """Raise the exception mirroring the reference taxonomy for status rc."""
     if rc == 0:

@@ -399,13 +399,31 @@ extern "C" int rdmm_fabric_create(const rdmm_fabric_config* cfg,
       return fail(RDMM_ERR_FABRIC, "control segment belongs to another fabric");
   }
   // pinned + device-mapped so kernels may observe control cells too
-  cudaHostRegister(mem, f->ctrl_map_bytes, cudaHostRegisterPortable);
-  cudaGetLastError();
+  // (skipped for control-plane-only fabrics: every local device < 0)
+  bool any_gpu = false;
+  for (uint32_t i = 0; i < cfg->nlocal; ++i)
+    any_gpu |= !cfg->devices || cfg->devices[i] >= 0;
+  if (any_gpu) {
+    cudaHostRegister(mem, f->ctrl_map_bytes, cudaHostRegisterPortable);
+    cudaGetLastError();
+  }
   // ---------------- local ranks: heaps, streams
   for (uint32_t i = 0; i < cfg->nlocal; ++i) {
     auto L = std::make_unique<Local>();
     L->rank = cfg->first_local + i;
     L->device = cfg->devices ? cfg->devices[i] : 0;
+    if (L->device < 0) {
+      // control-plane-only rank (no GPU): cells, queues, barrier, no heap
+      if (cfg->heap_bytes)
+        return fail(RDMM_ERR_FABRIC, "a rank without a device cannot have a heap");
+      RankSlot& rs = f->ctrl->ranks[L->rank];
+      rs.heap_bytes = 0;
+      rs.device = -1;
+      rs.pid = int32_t(getpid());
+      rs.published.store(1, std::memory_order_release);
+      f->locals.push_back(std::move(L));
+      continue;
+    }
     RDMM_CUDA_TRY(cudaSetDevice(L->device));
     void* hp = nullptr;
     RDMM_CUDA_TRY(cudaMalloc(&hp, cfg->heap_bytes ? cfg->heap_bytes : 8));
@@ -441,8 +459,10 @@ extern "C" int rdmm_fabric_create(const rdmm_fabric_config* cfg,
   f->base.assign(cfg->nlocal, std::vector<char*>(cfg->nranks, nullptr));
   for (uint32_t i = 0; i < cfg->nlocal; ++i) {
     Local* L = f->locals[i].get();
+    if (L->device < 0) continue;
     RDMM_CUDA_TRY(cudaSetDevice(L->device));
     for (uint32_t r = 0; r < cfg->nranks; ++r) {
+      if (f->ctrl->ranks[r].device < 0) continue;
       if (Local* R = f->local(r)) {
         if (R->device != L->device) {
           int can = 0;
@@ -487,6 +507,7 @@ extern "C" void rdmm_fabric_destroy(rdmm_fabric* f) {
     cudaIpcCloseMemHandle(p);
   }
   for (auto& L : f->locals) {
+    if (L->device < 0) continue;
     cudaSetDevice(L->device);
     for (auto s : L->streams)
       if (s) {
@@ -496,9 +517,13 @@ extern "C" void rdmm_fabric_destroy(rdmm_fabric* f) {
     if (L->heap.base) cudaFree(L->heap.base);
     if (L->atomic_slot) cudaFreeHost(L->atomic_slot);
   }
-  if (f->ctrl) {
+  bool any_gpu = false;
+  for (auto& L : f->locals) any_gpu |= L->device >= 0;
+  if (f->ctrl && any_gpu) {
     cudaHostUnregister(f->ctrl);
     cudaGetLastError();
+  }
+  if (f->ctrl) {
     munmap(f->ctrl, f->ctrl_map_bytes);
   }
   if (f->shared && f->owns_shm) shm_unlink(f->session.c_str());
@@ -827,8 +852,10 @@ extern "C" int rdmm_queue_pop(rdmm_fabric* f, uint32_t caller, uint64_t qid,
 extern "C" int rdmm_barrier(rdmm_fabric* f, uint32_t caller) {
   Local* C = f->local(caller);
   if (!C) return fail(RDMM_ERR_FABRIC, "caller rank not local");
-  cudaSetDevice(C->device);
-  for (auto s : C->streams) RDMM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (C->device >= 0) {
+    cudaSetDevice(C->device);
+    for (auto s : C->streams) RDMM_CUDA_TRY(cudaStreamSynchronize(s));
+  }
   return barrier_n(f, 1);
 }
 

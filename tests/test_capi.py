@@ -35,6 +35,23 @@ def test_cuda_capi_exports_every_declared_symbol():
         assert hasattr(lib, n)
 
 
+def test_host_capi_exports_every_declared_symbol():
+    import paper_2311_18141_b200._lib as L
+
+    names = declared("rdmm_host.h")
+    assert "rdmm_h_run_multiply" in names
+    syms = exported(L.LIB_PATH)
+    assert not [n for n in names if n not in syms]
+
+
+def test_fabric_capi_declared():
+    names = declared("rdmm_cuda.h")
+    for n in ("rdmm_fabric_create", "rdmm_get_nb", "rdmm_wait", "rdmm_fetch_add_i64",
+              "rdmm_queue_push", "rdmm_queue_pop", "rdmm_barrier", "rdmm_heap_alloc",
+              "rdmm_spgemm_symbolic", "rdmm_spgemm_numeric", "rdmm_spmm_csr_f32"):
+        assert n in names
+
+
 def test_error_taxonomy_mapping():
     import paper_2311_18141_b200 as rd
 
