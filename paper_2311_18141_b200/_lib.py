@@ -138,6 +138,10 @@ rdmm_queue_open = _fn("rdmm_queue_open", [vp, u32, u64, u64, P(u64)])
 rdmm_queue_push = _fn("rdmm_queue_push", [vp, u32, u64, Gptr, vp, u32])
 rdmm_queue_pop = _fn("rdmm_queue_pop", [vp, u32, u64, P(Gptr), vp, u32, P(cint)])
 rdmm_barrier = _fn("rdmm_barrier", [vp, u32])
+rdmm_heap_alloc = _fn("rdmm_heap_alloc", [vp, u32, u64, P(Gptr)])
+rdmm_gptr_device = _fn("rdmm_gptr_device", [vp, u32, Gptr, P(vp)])
+rdmm_memcpy = _fn("rdmm_memcpy", [vp, vp, u64, vp])
+rdmm_memset = _fn("rdmm_memset", [vp, cint, u64, vp])
 rdmm_fabric_abort = _fn("rdmm_fabric_abort", [vp, C.c_char_p], None)
 
 
