@@ -1,5 +1,6 @@
 // common.cu -- error plumbing and per-thread scratch for the C-ABI.
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -18,37 +19,38 @@ int fail(int code, const std::string& msg) {
 }
 
 namespace {
-struct Scratch {
-  struct Buf {
-    void* p = nullptr;
-    size_t n = 0;
-  };
-  // [device][slot]
-  std::vector<std::vector<Buf>> bufs;
-  ~Scratch() {
-    // Process teardown: the CUDA context may already be gone; leak quietly.
+struct ScratchKey {
+  int dev;
+  cudaStream_t stream;
+  int slot;
+  bool operator<(const ScratchKey& o) const {
+    if (dev != o.dev) return dev < o.dev;
+    if (stream != o.stream) return stream < o.stream;
+    return slot < o.slot;
   }
 };
-thread_local Scratch g_scratch;
+struct ScratchBuf {
+  void* p = nullptr;
+  size_t n = 0;
+};
+std::mutex g_scratch_mu;
+std::map<ScratchKey, ScratchBuf>& scratch_map() {
+  static auto* m = new std::map<ScratchKey, ScratchBuf>();  // never destroyed
+  return *m;
+}
 }  // namespace
 
-void* scratch(size_t bytes, int slot) {
+void* scratch(size_t bytes, int slot, cudaStream_t stream) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  auto& per = g_scratch.bufs;
-  if (per.size() <= size_t(dev)) per.resize(dev + 1);
-  auto& slots = per[dev];
-  if (slots.size() <= size_t(slot)) slots.resize(slot + 1);
-  auto& b = slots[slot];
-  if (b.n >= bytes) return b.p;
-  if (b.p) {
-    cudaDeviceSynchronize();  // in-flight kernels may still use the old one
-    cudaFree(b.p);
-    b.p = nullptr;
-    b.n = 0;
-  }
-  size_t n = bytes + bytes / 4 + 4096;
-  if (cudaMalloc(&b.p, n) != cudaSuccess) {
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  ScratchBuf& b = scratch_map()[ScratchKey{dev, stream, slot}];
+  if (b.n >= bytes && b.p) return b.p;
+  if (b.p) cudaFreeAsync(b.p, stream);
+  b.p = nullptr;
+  b.n = 0;
+  const size_t n = bytes + bytes / 4 + 4096;
+  if (cudaMallocAsync(&b.p, n, stream) != cudaSuccess) {
     cudaGetLastError();
     b.p = nullptr;
     return nullptr;

@@ -38,10 +38,11 @@ inline int num_sms() {
   return sms;
 }
 
-// Grow-only per-(thread, device) scratch used when the caller passes no
-// workspace.  Stream-ordered reuse: callers on one host thread serialise
-// their kernels on one stream per device (the algorithms in this library do).
-void* scratch(size_t bytes, int slot = 0);
+// Grow-only scratch per (device, stream, slot) used when the caller passes no
+// workspace.  Reuse is stream-ordered (all users of a buffer run on its
+// stream); growth frees/allocates on the stream (cudaFreeAsync /
+// cudaMallocAsync), so no host synchronisation is needed.
+void* scratch(size_t bytes, int slot, cudaStream_t stream);
 
 // Launch accounting for bench.py's gpu_launches claim (our kernels only).
 void count_launch(unsigned n = 1);

@@ -619,7 +619,7 @@ int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
   void* w = ws;
   if (!w || ws_bytes < P.bytes) {
     if (ws) return fail(RDMM_ERR_INVALID, "spmm: workspace too small");
-    w = scratch(P.bytes, 0);
+    w = scratch(P.bytes, 0, s);
     if (!w) return fail(RDMM_ERR_CUDA, "spmm: scratch allocation failed");
   }
   SpmmArgs<T> a{};

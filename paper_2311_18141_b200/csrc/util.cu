@@ -91,7 +91,7 @@ extern "C" int rdmm_csr_extract_count(const uint32_t* rp, const uint32_t* ci,
                                       uint32_t ncols, uint32_t* out_rp,
                                       uint64_t* nnz, rdmm_stream_t stream) {
   cudaStream_t s = as_stream(stream);
-  void* cnt = scratch(4ull * (nrows + 1), 1);
+  void* cnt = scratch(4ull * (nrows + 1), 1, s);
   if (!cnt) return fail(RDMM_ERR_CUDA, "extract: scratch allocation failed");
   const unsigned blocks = unsigned(std::max<uint64_t>(
       1, std::min<uint64_t>(ceil_div(nrows, 256), uint64_t(num_sms()) * 8)));
@@ -101,7 +101,7 @@ extern "C" int rdmm_csr_extract_count(const uint32_t* rp, const uint32_t* ci,
   size_t tb = 0;
   RDMM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, static_cast<uint32_t*>(cnt),
                                               out_rp, int64_t(nrows) + 1, s));
-  void* tmp = scratch(tb + 16, 2);
+  void* tmp = scratch(tb + 16, 2, s);
   if (!tmp) return fail(RDMM_ERR_CUDA, "extract: scratch allocation failed");
   RDMM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, static_cast<uint32_t*>(cnt),
                                               out_rp, int64_t(nrows) + 1, s));
@@ -138,7 +138,7 @@ extern "C" int rdmm_tile_sum(int dtype_bytes, uint32_t rows, uint32_t cols,
                              uint64_t ld, const void* p, rdmm_stream_t stream,
                              double* out) {
   cudaStream_t s = as_stream(stream);
-  double* d = static_cast<double*>(scratch(64, 3));
+  double* d = static_cast<double*>(scratch(64, 3, s));
   if (!d) return fail(RDMM_ERR_CUDA, "tile_sum: scratch allocation failed");
   RDMM_CUDA_TRY(cudaMemsetAsync(d, 0, 8, s));
   const uint64_t total = uint64_t(rows) * cols;
