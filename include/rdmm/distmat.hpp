@@ -450,19 +450,29 @@ class DistSparse {  // distmat.hpp:210-398
     ctx.barrier();
   }
 
-  // Bytes of the caller's owned tiles copied to host buffers (the
-  // device->host half of an end-to-end call); returns the bytes moved.
-  std::uint64_t owned_to_host(RankCtx& ctx, std::vector<char>& out) {
+  // Bytes of the caller's owned tiles (raw CSR arrays).
+  std::uint64_t owned_bytes(rank_t r) const {
+    std::uint64_t bytes = 0;
+    for (std::uint32_t i = 0; i < geom_.M; ++i)
+      for (std::uint32_t j = 0; j < geom_.N; ++j)
+        if (owner(i, j) == r) {
+          const Entry& e = dir_[geom_.idx(i, j)];
+          bytes += e.row_ptr.length + e.col_idx.length + e.values.length;
+        }
+    return bytes;
+  }
+  // Copy the caller's owned tiles (raw CSR arrays, concatenated) into a host
+  // buffer (the device->host half of an end-to-end call); returns bytes.
+  std::uint64_t owned_to_host(RankCtx& ctx, char* out, std::uint64_t cap) {
     std::uint64_t bytes = 0;
     for (std::uint32_t i = 0; i < geom_.M; ++i)
       for (std::uint32_t j = 0; j < geom_.N; ++j) {
         if (owner(i, j) != ctx.rank()) continue;
         const Entry& e = dir_[geom_.idx(i, j)];
         for (auto g : {e.row_ptr, e.col_idx, e.values}) {
-          const std::size_t o = out.size();
-          out.resize(o + g.length);
+          if (bytes + g.length > cap) throw std::invalid_argument("owned_to_host: buffer too small");
           if (g.length)
-            check(rdmm_memcpy(out.data() + o, fabric_->raw(GlobalPtr::of(g), ctx.rank()), g.length,
+            check(rdmm_memcpy(out + bytes, fabric_->raw(GlobalPtr::of(g), ctx.rank()), g.length,
                               ctx.stream(0)),
                   "owned_to_host");
           bytes += g.length;

@@ -55,9 +55,11 @@ int rdmm_h_dense_init(rdmm_h_matrix* mat, const void* global, uint64_t ld);
 int rdmm_h_dense_zero(rdmm_h_matrix* mat);
 /* End-to-end download: each local rank copies ITS tiles of the result into
  * the host array (dense: row-major global layout; sparse: the raw CSR arrays
- * of its tiles, concatenated, *bytes set to the amount moved). */
+ * of its tiles, concatenated into buf (capacity cap; pinned memory for
+ * full speed), *bytes set to the amount moved). */
 int rdmm_h_dense_owned_to_host(rdmm_h_matrix* mat, void* global, uint64_t ld);
-int rdmm_h_sparse_owned_to_host(rdmm_h_matrix* mat, uint64_t* bytes);
+int rdmm_h_sparse_owned_to_host(rdmm_h_matrix* mat, void* buf, uint64_t cap,
+                                uint64_t* bytes);
 /* The compute stream of a local rank (timing events go there). */
 void* rdmm_h_fabric_stream(rdmm_h_fabric* f, uint32_t rank);
 

@@ -103,23 +103,27 @@ struct Heap {
 
   static uint64_t align_up(uint64_t n) { return n == 0 ? 8 : (n + 7) & ~7ull; }
 
-  // fabric.hpp:284-303 first fit
+  // fabric.hpp:284-303 first fit, 8-byte granules; requests of >= 256
+  // bytes are additionally placed on 256-byte boundaries so device tiles
+  // keep the 16-byte alignment the vectorised kernels need (padding stays
+  // free and is reused by small requests).
   bool alloc(uint64_t nbytes, uint64_t* off) {
     std::lock_guard<std::mutex> lk(mu);
     const uint64_t need = align_up(nbytes);
-    for (auto it = free_list.begin(); it != free_list.end(); ++it) {
-      if (it->second >= need) {
-        *off = it->first;
-        if (it->second == need)
-          free_list.erase(it);
-        else {
-          it->first += need;
-          it->second -= need;
-        }
-        live[*off] = need;
-        remaining -= need;
-        return true;
-      }
+    const uint64_t align = need >= 256 ? 256 : 8;
+    for (std::size_t b = 0; b < free_list.size(); ++b) {
+      const uint64_t bo = free_list[b].first, bs = free_list[b].second;
+      const uint64_t start = (bo + align - 1) & ~(align - 1);
+      const uint64_t pad = start - bo;
+      if (bs < pad + need) continue;
+      free_list.erase(free_list.begin() + std::ptrdiff_t(b));
+      if (pad) free_list.push_back({bo, pad});
+      if (bs > pad + need) free_list.push_back({start + need, bs - pad - need});
+      std::sort(free_list.begin(), free_list.end());
+      *off = start;
+      live[start] = need;
+      remaining -= need;
+      return true;
     }
     return false;
   }

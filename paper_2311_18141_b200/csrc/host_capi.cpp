@@ -313,14 +313,24 @@ extern "C" int rdmm_h_dense_owned_to_host(rdmm_h_matrix* mat, void* global, uint
   });
 }
 
-extern "C" int rdmm_h_sparse_owned_to_host(rdmm_h_matrix* mat, uint64_t* bytes) {
+extern "C" int rdmm_h_sparse_owned_to_host(rdmm_h_matrix* mat, void* buf, uint64_t cap,
+                                           uint64_t* bytes) {
   return guarded([&] {
     if (mat->kind != 0) throw std::invalid_argument("not a sparse matrix");
     std::atomic<uint64_t> total{0};
     auto go = [&](auto& m) {
+      // local ranks write disjoint consecutive slices of buf
+      std::vector<uint64_t> off(mat->fab->f->nlocal() + 1, 0);
+      for (rank_t i = 0; i < mat->fab->f->nlocal(); ++i)
+        off[i + 1] = off[i] + m.owned_bytes(mat->fab->f->first_local() + i);
+      if (!buf) {
+        total = off.back();
+        return;
+      }
+      if (off.back() > cap) throw std::invalid_argument("owned_to_host: buffer too small");
       run_ranks(*mat->fab->f, [&](RankCtx& ctx) {
-        std::vector<char> buf;
-        total += m.owned_to_host(ctx, buf);
+        const rank_t i = ctx.rank() - mat->fab->f->first_local();
+        total += m.owned_to_host(ctx, static_cast<char*>(buf) + off[i], off[i + 1] - off[i]);
       });
     };
     if (mat->dtype == 8)

@@ -61,7 +61,7 @@ _h.rdmm_h_dense_zero.argtypes = [_vp]
 _h.rdmm_h_dense_zero.restype = _int
 _h.rdmm_h_dense_owned_to_host.argtypes = [_vp, _vp, _u64]
 _h.rdmm_h_dense_owned_to_host.restype = _int
-_h.rdmm_h_sparse_owned_to_host.argtypes = [_vp, C.POINTER(_u64)]
+_h.rdmm_h_sparse_owned_to_host.argtypes = [_vp, _vp, _u64, C.POINTER(_u64)]
 _h.rdmm_h_sparse_owned_to_host.restype = _int
 _h.rdmm_h_fabric_stream.argtypes = [_vp, _u32]
 _h.rdmm_h_fabric_stream.restype = _vp
@@ -199,10 +199,18 @@ class DistSparse(_Mat):
                                       dcsr.values.data_ptr() if dcsr.nnz else None, dcsr.nnz, 1),
                 "init_from_device")
 
-    def owned_to_host(self):
-        """D2H of this process's tiles (raw CSR arrays); returns bytes."""
+    def owned_bytes(self):
         n = C.c_uint64(0)
-        L.check(_h.rdmm_h_sparse_owned_to_host(self._h, C.byref(n)), "owned_to_host")
+        L.check(_h.rdmm_h_sparse_owned_to_host(self._h, None, 0, C.byref(n)), "owned_bytes")
+        return n.value
+
+    def owned_to_host(self, buf):
+        """D2H of this process's tiles (raw CSR arrays) into `buf` (a pinned
+        uint8 tensor or numpy array); returns bytes moved."""
+        ptr = buf.data_ptr() if hasattr(buf, "data_ptr") else buf.ctypes.data
+        cap = buf.numel() if hasattr(buf, "numel") else buf.nbytes
+        n = C.c_uint64(0)
+        L.check(_h.rdmm_h_sparse_owned_to_host(self._h, ptr, cap, C.byref(n)), "owned_to_host")
         return n.value
 
     def nnz(self):
