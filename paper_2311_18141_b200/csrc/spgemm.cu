@@ -21,6 +21,7 @@
 // prefix-summed over their B-row lengths and the group's threads take
 // consecutive products, so B rows are read coalesced and hub rows of R-MAT
 // do not serialise on one thread.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -125,7 +126,8 @@ template <typename T, int G, bool kValues, class Ins>
 __device__ __forceinline__ void enumerate_row(uint32_t r,
                                               const TermDev<T>* terms,
                                               int nterms, Win<T, G>& w,
-                                              Ins ins) {
+                                              Ins ins, uint32_t part = 0,
+                                              uint32_t nparts = 1) {
   const uint32_t tg = threadIdx.x % G;
   for (int t = 0; t < nterms; ++t) {
     const TermDev<T> tm = terms[t];
@@ -149,7 +151,7 @@ __device__ __forceinline__ void enumerate_row(uint32_t r,
       if (kValues) w.a[tg] = a;
       gsync<G>();
       const uint32_t nvalid = min(uint32_t(G), s1 - base);
-      for (uint32_t p = tg; p < total; p += G) {
+      for (uint32_t p = tg + part * G; p < total; p += nparts * G) {
         uint32_t lo = 0, hi = nvalid;
         while (hi - lo > 1) {
           const uint32_t mid = (lo + hi) >> 1;
@@ -351,72 +353,79 @@ __global__ void __launch_bounds__(G == 32 ? 256 : G)
 }
 
 // ------------------------------------------------------------ dense tier
+//
+// Rows whose output does not fit a shared-memory table are accumulated in a
+// dense value array + bitmap over all columns.  A thread-block CLUSTER of
+// kCluster CTAs owns one row at a time (the products are interleaved over
+// the cluster's CTAs), so only gridDim/kCluster rows are in flight and their
+// accumulators (n floats + n bits each) stay resident in the 126 MB L2; the
+// in-order bitmap scan, split over the cluster with the per-CTA counts
+// exchanged through distributed shared memory, emits sorted columns.
+constexpr int kCluster = 8;
 
-template <typename T>
-__global__ void __launch_bounds__(kDenseThreads)
-    k_sym_dense(const uint32_t* __restrict__ list, uint32_t count,
-                const TermDev<T>* terms, int nterms, uint64_t* cnt64,
-                uint32_t* bitmaps, uint32_t nwords) {
+template <typename T, bool kNumeric>
+__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kDenseThreads)
+    k_dense_cluster(const uint32_t* __restrict__ list, uint32_t count,
+                    const TermDev<T>* terms, int nterms, uint64_t* cnt64,
+                    const uint32_t* __restrict__ crp, uint32_t* __restrict__ cci,
+                    T* __restrict__ cv, uint32_t* bitmaps, T* dense, uint32_t nwords,
+                    uint32_t ncols, T ident_val) {
   constexpr int G = kDenseThreads;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
   __shared__ Win<T, G> win;
-  uint32_t* bm = bitmaps + size_t(blockIdx.x) * nwords;
-  for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
+  __shared__ uint32_t slice_count;
+  const uint32_t part = cluster.block_rank();
+  const uint32_t cid = blockIdx.x / kCluster, ncl = gridDim.x / kCluster;
+  uint32_t* bm = bitmaps + size_t(cid) * nwords;
+  T* dv = kNumeric ? dense + size_t(cid) * ncols : nullptr;
+  // this CTA's slice of the bitmap words, and each thread's part of it
+  const uint32_t wper = (nwords + kCluster - 1) / kCluster;
+  const uint32_t ws0 = min(part * wper, nwords), ws1 = min(ws0 + wper, nwords);
+  const uint32_t tper = (ws1 - ws0 + G - 1) / G;
+  const uint32_t w0 = min(ws0 + threadIdx.x * tper, ws1), w1 = min(w0 + tper, ws1);
+  for (uint32_t li = cid; li < count; li += ncl) {
     const uint32_t r = list[li];
-    enumerate_row<T, G, false>(r, terms, nterms, win, [&](uint32_t key, T) {
-      const uint32_t bit = 1u << (key & 31);
-      if (!(bm[key >> 5] & bit)) atomicOr(bm + (key >> 5), bit);
-    });
-    __syncthreads();
+    enumerate_row<T, G, kNumeric>(
+        r, terms, nterms, win,
+        [&](uint32_t key, T v) {
+          const uint32_t bit = 1u << (key & 31);
+          if (!(__ldcg(bm + (key >> 5)) & bit)) atomicOr(bm + (key >> 5), bit);
+          if constexpr (kNumeric) atomicAdd(dv + key, v);
+        },
+        part, kCluster);
+    __threadfence();
+    cluster.sync();
     uint32_t c = 0;
-    for (uint32_t i = threadIdx.x; i < nwords; i += G) {
-      c += __popc(bm[i]);
-      bm[i] = 0;
-    }
-    c = gsum<G>(c, win.sums);
-    if (threadIdx.x == 0) cnt64[r] = c;
-    __syncthreads();
-  }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kDenseThreads)
-    k_num_dense(const uint32_t* __restrict__ list, uint32_t count,
-                const TermDev<T>* terms, int nterms,
-                const uint32_t* __restrict__ crp, uint32_t* __restrict__ cci,
-                T* __restrict__ cv, uint32_t* bitmaps, T* dense,
-                uint32_t nwords, uint32_t ncols, T ident_val) {
-  constexpr int G = kDenseThreads;
-  __shared__ Win<T, G> win;
-  uint32_t* bm = bitmaps + size_t(blockIdx.x) * nwords;
-  T* dv = dense + size_t(blockIdx.x) * ncols;
-  const uint32_t per = (nwords + G - 1) / G;
-  for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
-    const uint32_t r = list[li];
-    enumerate_row<T, G, true>(r, terms, nterms, win, [&](uint32_t key, T v) {
-      const uint32_t bit = 1u << (key & 31);
-      if (!(bm[key >> 5] & bit)) atomicOr(bm + (key >> 5), bit);
-      atomicAdd(dv + key, v);
-    });
-    __syncthreads();
-    const uint32_t w0 = threadIdx.x * per, w1 = min(w0 + per, nwords);
-    uint32_t c = 0;
-    for (uint32_t w = w0; w < w1; ++w) c += __popc(bm[w]);
+    for (uint32_t w = w0; w < w1; ++w) c += __popc(__ldcg(bm + w));
     uint32_t total;
-    uint32_t pos = crp[r] + gscan<G>(c, win.sums, total);
-    for (uint32_t w = w0; w < w1; ++w) {
-      uint32_t bits = bm[w];
-      bm[w] = 0;
-      while (bits) {
-        const uint32_t b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const uint32_t col = w * 32 + b;
-        cci[pos] = col;
-        cv[pos] = dv[col];
-        dv[col] = ident_val;
-        ++pos;
+    uint32_t off = gscan<G>(c, win.sums, total);
+    if constexpr (!kNumeric) {
+      for (uint32_t w = w0; w < w1; ++w) bm[w] = 0;
+      if (threadIdx.x == 0 && total) atomicAdd(reinterpret_cast<unsigned long long*>(cnt64 + r),
+                                                 (unsigned long long)total);
+    } else {
+      if (threadIdx.x == 0) slice_count = total;
+      cluster.sync();
+      uint32_t base = 0;
+      for (uint32_t q = 0; q < part; ++q) base += *cluster.map_shared_rank(&slice_count, q);
+      uint32_t pos = crp[r] + base + off;
+      for (uint32_t w = w0; w < w1; ++w) {
+        uint32_t bits = __ldcg(bm + w);
+        bm[w] = 0;
+        while (bits) {
+          const uint32_t b = __ffs(bits) - 1;
+          bits &= bits - 1;
+          const uint32_t col = w * 32 + b;
+          cci[pos] = col;
+          cv[pos] = __ldcg(dv + col);
+          dv[col] = ident_val;
+          ++pos;
+        }
       }
     }
-    __syncthreads();
+    __threadfence();
+    cluster.sync();
   }
 }
 
@@ -431,6 +440,12 @@ __global__ void k_rowptr32(const uint64_t* pre, uint32_t n1, uint32_t* rp) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n1;
        i += gridDim.x * blockDim.x)
     rp[i] = uint32_t(pre[i]);
+}
+
+// Concurrent dense rows (clusters): enough to fill the SMs, few enough that
+// their accumulators stay in L2.
+inline uint32_t dense_clusters(uint32_t rows) {
+  return std::max<uint32_t>(1, std::min<uint32_t>(rows, uint32_t(num_sms()) / kCluster));
 }
 
 struct Buf {
@@ -591,12 +606,13 @@ int symbolic_impl(uint32_t rows, uint32_t ncols, const rdmm_spgemm_term* terms,
   if (rc) return rc;
   const uint32_t nwords = uint32_t(ceil_div(ncols, 32));
   if (hc[5]) {
-    const uint32_t blocks = std::min<uint32_t>(hc[5], uint32_t(num_sms()));
-    RDMM_CUDA_TRY(P->bitmaps.ensure(size_t(blocks) * nwords * 4));
-    RDMM_CUDA_TRY(cudaMemsetAsync(P->bitmaps.p, 0, size_t(blocks) * nwords * 4, s));
+    const uint32_t ncl = dense_clusters(hc[5]);
+    RDMM_CUDA_TRY(P->bitmaps.ensure(size_t(ncl) * nwords * 4));
+    RDMM_CUDA_TRY(cudaMemsetAsync(P->bitmaps.p, 0, size_t(ncl) * nwords * 4, s));
     count_launch();
-    k_sym_dense<T><<<blocks, kDenseThreads, 0, s>>>(
-        L(5), hc[5], td, nterms, cnt, P->bitmaps.as<uint32_t>(), nwords);
+    k_dense_cluster<T, false><<<ncl * kCluster, kDenseThreads, 0, s>>>(
+        L(5), hc[5], td, nterms, cnt, nullptr, nullptr, nullptr, P->bitmaps.as<uint32_t>(),
+        nullptr, nwords, ncols, T(0));
   }
   RDMM_CUDA_TRY(cudaGetLastError());
   // row_ptr = exclusive scan of the counts (64-bit, checked against uint32)
@@ -661,7 +677,7 @@ int numeric_impl(rdmm_spgemm_plan* P, uint32_t* cci, T* cv, cudaStream_t s) {
   if (rc) return rc;
   if (c[5]) {
     const uint32_t nwords = uint32_t(ceil_div(P->ncols, 32));
-    const uint32_t blocks = std::min<uint32_t>(c[5], uint32_t(num_sms()));
+    const uint32_t blocks = dense_clusters(c[5]);
     RDMM_CUDA_TRY(P->bitmaps.ensure(size_t(blocks) * nwords * 4));
     RDMM_CUDA_TRY(cudaMemsetAsync(P->bitmaps.p, 0, size_t(blocks) * nwords * 4, s));
     RDMM_CUDA_TRY(P->dense.ensure(size_t(blocks) * P->ncols * sizeof(T)));
@@ -670,8 +686,8 @@ int numeric_impl(rdmm_spgemm_plan* P, uint32_t* cci, T* cv, cudaStream_t s) {
     k_fill<T><<<unsigned(std::min<uint64_t>(ceil_div(nd, 256), 4096)), 256, 0, s>>>(
         P->dense.as<T>(), nd, ident);
     count_launch();
-    k_num_dense<T><<<blocks, kDenseThreads, 0, s>>>(
-        L(5), c[5], td, nt, crp, cci, cv, P->bitmaps.as<uint32_t>(),
+    k_dense_cluster<T, true><<<blocks * kCluster, kDenseThreads, 0, s>>>(
+        L(5), c[5], td, nt, nullptr, crp, cci, cv, P->bitmaps.as<uint32_t>(),
         P->dense.as<T>(), nwords, P->ncols, ident);
   }
   RDMM_CUDA_TRY(cudaGetLastError());
