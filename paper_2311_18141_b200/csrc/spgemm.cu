@@ -25,6 +25,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -282,12 +283,24 @@ __global__ void __launch_bounds__(G == 32 ? 256 : G)
   }
 }
 
+// Bytes of the numeric table region: keys + values, or the block radix
+// sort's scratch that aliases it, whichever is larger.
+template <typename T, int TAB, int G>
+constexpr size_t num_table_bytes() {
+  if constexpr (G == 32) {
+    return size_t(TAB) * (sizeof(T) + 4);
+  } else {
+    using BRS = cub::BlockRadixSort<uint32_t, G, TAB / G, T>;
+    return std::max(size_t(TAB) * (sizeof(T) + 4), sizeof(typename BRS::TempStorage));
+  }
+}
+
 template <typename T, int TAB, int G>
 __global__ void __launch_bounds__(G == 32 ? 256 : G)
     k_num_hash(const uint32_t* __restrict__ list, uint32_t count,
                const TermDev<T>* terms, int nterms,
                const uint32_t* __restrict__ crp, uint32_t* __restrict__ cci,
-               T* __restrict__ cv, T ident_val) {
+               T* __restrict__ cv, T ident_val, int key_bits) {
   constexpr int RPB = G == 32 ? 8 : 1;
   constexpr int LOG2T = __builtin_ctz(TAB);
   extern __shared__ __align__(16) unsigned char smem[];
@@ -297,7 +310,7 @@ __global__ void __launch_bounds__(G == 32 ? 256 : G)
       reinterpret_cast<uint32_t*>(smem + size_t(RPB) * TAB * sizeof(T)) +
       size_t(grp) * TAB;
   Win<T, G>* win = reinterpret_cast<Win<T, G>*>(
-      smem + size_t(RPB) * TAB * (sizeof(T) + 4)) + grp;
+      smem + size_t(RPB) * num_table_bytes<T, TAB, G>()) + grp;
   for (uint32_t li = blockIdx.x * RPB + grp; li - grp < count;
        li += gridDim.x * RPB) {
     const bool active = li < count;
@@ -321,113 +334,229 @@ __global__ void __launch_bounds__(G == 32 ? 256 : G)
         atomicAdd(vals + s, v);
       });
     gsync<G>();
-    // bitonic sort (keys, vals) ascending; empty keys sort last
-    for (uint32_t k = 2; k <= uint32_t(TAB); k <<= 1) {
-      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-        for (uint32_t i = tg; i < uint32_t(TAB); i += G) {
-          const uint32_t ixj = i ^ j;
-          if (ixj > i) {
-            const uint32_t ki = keys[i], kj = keys[ixj];
-            const bool up = (i & k) == 0;
-            if ((ki > kj) == up) {
-              keys[i] = kj;
-              keys[ixj] = ki;
-              const T t = vals[i];
-              vals[i] = vals[ixj];
-              vals[ixj] = t;
+    if constexpr (G == 32) {
+      // warp tier: bitonic sort of the 64-slot table; empty keys sort last
+      for (uint32_t k = 2; k <= uint32_t(TAB); k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+          for (uint32_t i = tg; i < uint32_t(TAB); i += G) {
+            const uint32_t ixj = i ^ j;
+            if (ixj > i) {
+              const uint32_t ki = keys[i], kj = keys[ixj];
+              const bool up = (i & k) == 0;
+              if ((ki > kj) == up) {
+                keys[i] = kj;
+                keys[ixj] = ki;
+                const T t = vals[i];
+                vals[i] = vals[ixj];
+                vals[ixj] = t;
+              }
             }
           }
+          gsync<G>();
         }
-        gsync<G>();
       }
-    }
-    if (active) {
-      const uint32_t o = crp[r], n = crp[r + 1] - o;
-      for (uint32_t i = tg; i < n; i += G) {
-        cci[o + i] = keys[i];
-        cv[o + i] = vals[i];
+      if (active) {
+        const uint32_t o = crp[r], n = crp[r + 1] - o;
+        for (uint32_t i = tg; i < n; i += G) {
+          cci[o + i] = keys[i];
+          cv[o + i] = vals[i];
+        }
       }
+      gsync<G>();
+    } else {
+      // CTA tiers: block radix sort of the whole table by column (bits
+      // [0, key_bits)); the empty key has all of those bits set, so it sorts
+      // after every real column.  The sort's scratch aliases the table.
+      constexpr int IPT = TAB / G;
+      using BRS = cub::BlockRadixSort<uint32_t, G, IPT, T>;
+      uint32_t kk[IPT];
+      T vv[IPT];
+#pragma unroll
+      for (int i = 0; i < IPT; ++i) {
+        kk[i] = keys[tg * IPT + i];
+        vv[i] = vals[tg * IPT + i];
+      }
+      __syncthreads();
+      BRS(*reinterpret_cast<typename BRS::TempStorage*>(smem)).Sort(kk, vv, 0, key_bits);
+      if (active) {
+        const uint32_t o = crp[r], n = crp[r + 1] - o;
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          const uint32_t idx = tg * IPT + i;
+          if (idx < n) {
+            cci[o + idx] = kk[i];
+            cv[o + idx] = vv[i];
+          }
+        }
+      }
+      __syncthreads();
     }
-    gsync<G>();
   }
 }
 
 // ------------------------------------------------------------ dense tier
 //
-// Rows whose output does not fit a shared-memory table are accumulated in a
-// dense value array + bitmap over all columns.  A thread-block CLUSTER of
-// kCluster CTAs owns one row at a time (the products are interleaved over
-// the cluster's CTAs), so only gridDim/kCluster rows are in flight and their
-// accumulators (n floats + n bits each) stay resident in the 126 MB L2; the
-// in-order bitmap scan, split over the cluster with the per-CTA counts
-// exchanged through distributed shared memory, emits sorted columns.
-constexpr int kCluster = 8;
+// Rows whose output does not fit a shared-memory table accumulate in a dense
+// value array + bitmap over all columns (global memory, per row slot).  CL
+// CTAs (a thread-block cluster when CL > 1) share one row: its products are
+// interleaved over the CTAs, and the in-order bitmap scan that emits sorted
+// columns is split over them with the per-CTA counts exchanged through
+// distributed shared memory.  R-MAT rows have hot output columns (thousands
+// of products per column), so every CTA first combines products in a
+// shared-memory write-combining cache (direct-mapped, CAS-claimed slots) and
+// only misses and the final flush reach the global array with atomics.
+// The symbolic pass keeps the whole bitmap in shared memory when it fits.
+constexpr int kWc = 8192;  // write-combining slots per CTA
 
-template <typename T, bool kNumeric>
-__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kDenseThreads)
-    k_dense_cluster(const uint32_t* __restrict__ list, uint32_t count,
-                    const TermDev<T>* terms, int nterms, uint64_t* cnt64,
-                    const uint32_t* __restrict__ crp, uint32_t* __restrict__ cci,
-                    T* __restrict__ cv, uint32_t* bitmaps, T* dense, uint32_t nwords,
-                    uint32_t ncols, T ident_val) {
+template <typename T>
+constexpr size_t dense_smem_bytes() {
+  return size_t(kWc) * (4 + sizeof(T));
+}
+
+template <typename T, int CL>
+__global__ void __launch_bounds__(kDenseThreads)
+    k_dense_num(const uint32_t* __restrict__ list, uint32_t count,
+                const TermDev<T>* terms, int nterms,
+                const uint32_t* __restrict__ crp, uint32_t* __restrict__ cci,
+                T* __restrict__ cv, uint32_t* bitmaps, T* dense, uint32_t nwords,
+                uint32_t ncols, T ident_val) {
   constexpr int G = kDenseThreads;
+  constexpr int LOG2W = __builtin_ctz(kWc);
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char dsm[];
+  uint32_t* wkey = reinterpret_cast<uint32_t*>(dsm);
+  T* wval = reinterpret_cast<T*>(dsm + size_t(kWc) * 4);
   __shared__ Win<T, G> win;
   __shared__ uint32_t slice_count;
-  const uint32_t part = cluster.block_rank();
-  const uint32_t cid = blockIdx.x / kCluster, ncl = gridDim.x / kCluster;
+  const uint32_t part = CL > 1 ? cluster.block_rank() : 0;
+  const uint32_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   uint32_t* bm = bitmaps + size_t(cid) * nwords;
-  T* dv = kNumeric ? dense + size_t(cid) * ncols : nullptr;
-  // this CTA's slice of the bitmap words, and each thread's part of it
-  const uint32_t wper = (nwords + kCluster - 1) / kCluster;
+  T* dv = dense + size_t(cid) * ncols;
+  const uint32_t wper = (nwords + CL - 1) / CL;
   const uint32_t ws0 = min(part * wper, nwords), ws1 = min(ws0 + wper, nwords);
   const uint32_t tper = (ws1 - ws0 + G - 1) / G;
   const uint32_t w0 = min(ws0 + threadIdx.x * tper, ws1), w1 = min(w0 + tper, ws1);
+  for (uint32_t i = threadIdx.x; i < kWc; i += G) {
+    wkey[i] = kEmpty;
+    wval[i] = ident_val;
+  }
+  __syncthreads();
   for (uint32_t li = cid; li < count; li += ncl) {
     const uint32_t r = list[li];
-    enumerate_row<T, G, kNumeric>(
+    enumerate_row<T, G, true>(
         r, terms, nterms, win,
         [&](uint32_t key, T v) {
           const uint32_t bit = 1u << (key & 31);
           if (!(__ldcg(bm + (key >> 5)) & bit)) atomicOr(bm + (key >> 5), bit);
-          if constexpr (kNumeric) atomicAdd(dv + key, v);
+          const uint32_t sl = hslot(key, LOG2W);
+          const uint32_t old = atomicCAS(wkey + sl, kEmpty, key);
+          if (old == kEmpty || old == key)
+            atomicAdd(wval + sl, v);
+          else
+            atomicAdd(dv + key, v);
         },
-        part, kCluster);
-    __threadfence();
-    cluster.sync();
-    uint32_t c = 0;
-    for (uint32_t w = w0; w < w1; ++w) c += __popc(__ldcg(bm + w));
-    uint32_t total;
-    uint32_t off = gscan<G>(c, win.sums, total);
-    if constexpr (!kNumeric) {
-      for (uint32_t w = w0; w < w1; ++w) bm[w] = 0;
-      if (threadIdx.x == 0 && total) atomicAdd(reinterpret_cast<unsigned long long*>(cnt64 + r),
-                                                 (unsigned long long)total);
-    } else {
-      if (threadIdx.x == 0) slice_count = total;
-      cluster.sync();
-      uint32_t base = 0;
-      for (uint32_t q = 0; q < part; ++q) base += *cluster.map_shared_rank(&slice_count, q);
-      uint32_t pos = crp[r] + base + off;
-      for (uint32_t w = w0; w < w1; ++w) {
-        uint32_t bits = __ldcg(bm + w);
-        bm[w] = 0;
-        while (bits) {
-          const uint32_t b = __ffs(bits) - 1;
-          bits &= bits - 1;
-          const uint32_t col = w * 32 + b;
-          cci[pos] = col;
-          cv[pos] = __ldcg(dv + col);
-          dv[col] = ident_val;
-          ++pos;
-        }
+        part, CL);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < kWc; i += G) {  // flush the cache
+      const uint32_t key = wkey[i];
+      if (key != kEmpty) {
+        atomicAdd(dv + key, wval[i]);
+        wkey[i] = kEmpty;
+        wval[i] = ident_val;
       }
     }
     __threadfence();
-    cluster.sync();
+    if constexpr (CL > 1) cluster.sync(); else __syncthreads();
+    uint32_t c = 0;
+    for (uint32_t w = w0; w < w1; ++w) c += __popc(__ldcg(bm + w));
+    uint32_t total;
+    const uint32_t off = gscan<G>(c, win.sums, total);
+    uint32_t base = 0;
+    if constexpr (CL > 1) {
+      if (threadIdx.x == 0) slice_count = total;
+      cluster.sync();
+      for (uint32_t q = 0; q < part; ++q) base += *cluster.map_shared_rank(&slice_count, q);
+    }
+    uint32_t pos = crp[r] + base + off;
+    for (uint32_t w = w0; w < w1; ++w) {
+      uint32_t bits = __ldcg(bm + w);
+      if (!bits) continue;
+      bm[w] = 0;
+      while (bits) {
+        const uint32_t b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const uint32_t col = w * 32 + b;
+        cci[pos] = col;
+        cv[pos] = __ldcg(dv + col);
+        dv[col] = ident_val;
+        ++pos;
+      }
+    }
+    __threadfence();
+    if constexpr (CL > 1) cluster.sync(); else __syncthreads();
   }
 }
+
+// Symbolic heavy rows: the column bitmap lives in shared memory (ncols bits).
+template <typename T>
+__global__ void __launch_bounds__(kDenseThreads)
+    k_dense_sym_smem(const uint32_t* __restrict__ list, uint32_t count,
+                     const TermDev<T>* terms, int nterms, uint64_t* cnt64, uint32_t nwords) {
+  constexpr int G = kDenseThreads;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  uint32_t* bm = reinterpret_cast<uint32_t*>(dsm);
+  __shared__ Win<T, G> win;
+  for (uint32_t i = threadIdx.x; i < nwords; i += G) bm[i] = 0;
+  __syncthreads();
+  for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
+    const uint32_t r = list[li];
+    enumerate_row<T, G, false>(r, terms, nterms, win, [&](uint32_t key, T) {
+      const uint32_t bit = 1u << (key & 31);
+      if (!(bm[key >> 5] & bit)) atomicOr(bm + (key >> 5), bit);
+    });
+    __syncthreads();
+    uint32_t c = 0;
+    for (uint32_t i = threadIdx.x; i < nwords; i += G) {
+      c += __popc(bm[i]);
+      bm[i] = 0;
+    }
+    c = gsum<G>(c, win.sums);
+    if (threadIdx.x == 0) cnt64[r] = c;
+    __syncthreads();
+  }
+}
+
+// Symbolic heavy rows when the bitmap does not fit shared memory.
+template <typename T>
+__global__ void __launch_bounds__(kDenseThreads)
+    k_dense_sym_global(const uint32_t* __restrict__ list, uint32_t count,
+                       const TermDev<T>* terms, int nterms, uint64_t* cnt64,
+                       uint32_t* bitmaps, uint32_t nwords) {
+  constexpr int G = kDenseThreads;
+  __shared__ Win<T, G> win;
+  uint32_t* bm = bitmaps + size_t(blockIdx.x) * nwords;
+  for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
+    const uint32_t r = list[li];
+    enumerate_row<T, G, false>(r, terms, nterms, win, [&](uint32_t key, T) {
+      const uint32_t bit = 1u << (key & 31);
+      if (!(__ldcg(bm + (key >> 5)) & bit)) atomicOr(bm + (key >> 5), bit);
+    });
+    __threadfence();
+    __syncthreads();
+    uint32_t c = 0;
+    for (uint32_t i = threadIdx.x; i < nwords; i += G) {
+      c += __popc(__ldcg(bm + i));
+      bm[i] = 0;
+    }
+    c = gsum<G>(c, win.sums);
+    if (threadIdx.x == 0) cnt64[r] = c;
+    __threadfence();
+    __syncthreads();
+  }
+}
+
+constexpr size_t kSymSmemMax = 200 * 1024;  // bitmap bytes kept in shared memory
 
 template <typename T>
 __global__ void k_fill(T* p, size_t n, T v) {
@@ -442,10 +571,44 @@ __global__ void k_rowptr32(const uint64_t* pre, uint32_t n1, uint32_t* rp) {
     rp[i] = uint32_t(pre[i]);
 }
 
-// Concurrent dense rows (clusters): enough to fill the SMs, few enough that
-// their accumulators stay in L2.
-inline uint32_t dense_clusters(uint32_t rows) {
-  return std::max<uint32_t>(1, std::min<uint32_t>(rows, uint32_t(num_sms()) / kCluster));
+// CTAs per dense row (RDMM_SPGEMM_CL, default 1: more rows in flight spread
+// the hot-column atomics over more addresses).
+inline int dense_cl() {
+  static const int v = [] {
+    const char* e = std::getenv("RDMM_SPGEMM_CL");
+    const int x = e ? std::atoi(e) : 1;
+    return x == 8 ? 8 : x == 4 ? 4 : x == 2 ? 2 : 1;
+  }();
+  return v;
+}
+inline uint32_t dense_rows_in_flight(uint32_t rows, int cl) {
+  return std::max<uint32_t>(1, std::min<uint32_t>(rows, uint32_t(num_sms()) / cl));
+}
+
+template <typename T, int CL>
+int launch_dense_num(uint32_t slots, const uint32_t* list, uint32_t count,
+                     const TermDev<T>* td, int nt, const uint32_t* crp, uint32_t* cci, T* cv,
+                     uint32_t* bm, T* dense, uint32_t nwords, uint32_t ncols, T ident,
+                     cudaStream_t s) {
+  auto fn = k_dense_num<T, CL>;
+  const size_t sm = dense_smem_bytes<T>();
+  RDMM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(slots * CL);
+  cfg.blockDim = dim3(kDenseThreads);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  count_launch();
+  RDMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, list, count, td, nt, crp, cci, cv, bm, dense,
+                                   nwords, ncols, ident));
+  return RDMM_OK;
 }
 
 struct Buf {
@@ -472,7 +635,7 @@ struct Buf {
 template <typename T, int TAB, int G>
 size_t hash_smem(bool numeric) {
   constexpr int RPB = G == 32 ? 8 : 1;
-  return size_t(RPB) * TAB * (numeric ? sizeof(T) + 4 : 4) +
+  return size_t(RPB) * (numeric ? num_table_bytes<T, TAB, G>() : size_t(TAB) * 4) +
          size_t(RPB) * sizeof(Win<T, G>);
 }
 
@@ -498,7 +661,7 @@ int launch_sym_hash(const uint32_t* list, uint32_t count,
 template <typename T, int TAB, int G>
 int launch_num_hash(const uint32_t* list, uint32_t count,
                     const TermDev<T>* terms, int nterms, const uint32_t* crp,
-                    uint32_t* cci, T* cv, T ident, cudaStream_t s) {
+                    uint32_t* cci, T* cv, T ident, int key_bits, cudaStream_t s) {
   if (!count) return 0;
   constexpr int RPB = G == 32 ? 8 : 1;
   const size_t sm = hash_smem<T, TAB, G>(true);
@@ -511,7 +674,7 @@ int launch_num_hash(const uint32_t* list, uint32_t count,
                                              uint64_t(num_sms()) * 64);
   count_launch();
   fn<<<unsigned(blocks), threads, sm, s>>>(list, count, terms, nterms, crp,
-                                           cci, cv, ident);
+                                           cci, cv, ident, key_bits);
   return 0;
 }
 
@@ -606,13 +769,20 @@ int symbolic_impl(uint32_t rows, uint32_t ncols, const rdmm_spgemm_term* terms,
   if (rc) return rc;
   const uint32_t nwords = uint32_t(ceil_div(ncols, 32));
   if (hc[5]) {
-    const uint32_t ncl = dense_clusters(hc[5]);
-    RDMM_CUDA_TRY(P->bitmaps.ensure(size_t(ncl) * nwords * 4));
-    RDMM_CUDA_TRY(cudaMemsetAsync(P->bitmaps.p, 0, size_t(ncl) * nwords * 4, s));
-    count_launch();
-    k_dense_cluster<T, false><<<ncl * kCluster, kDenseThreads, 0, s>>>(
-        L(5), hc[5], td, nterms, cnt, nullptr, nullptr, nullptr, P->bitmaps.as<uint32_t>(),
-        nullptr, nwords, ncols, T(0));
+    const uint32_t blocks = dense_rows_in_flight(hc[5], 1);
+    if (size_t(nwords) * 4 <= kSymSmemMax) {
+      auto fn = k_dense_sym_smem<T>;
+      RDMM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(nwords * 4)));
+      count_launch();
+      fn<<<blocks, kDenseThreads, nwords * 4, s>>>(L(5), hc[5], td, nterms, cnt, nwords);
+    } else {
+      RDMM_CUDA_TRY(P->bitmaps.ensure(size_t(blocks) * nwords * 4));
+      RDMM_CUDA_TRY(cudaMemsetAsync(P->bitmaps.p, 0, size_t(blocks) * nwords * 4, s));
+      count_launch();
+      k_dense_sym_global<T><<<blocks, kDenseThreads, 0, s>>>(
+          L(5), hc[5], td, nterms, cnt, P->bitmaps.as<uint32_t>(), nwords);
+    }
   }
   RDMM_CUDA_TRY(cudaGetLastError());
   // row_ptr = exclusive scan of the counts (64-bit, checked against uint32)
@@ -668,16 +838,21 @@ int numeric_impl(rdmm_spgemm_plan* P, uint32_t* cci, T* cv, cudaStream_t s) {
   KernelTimer timer(s, 2);
   const uint32_t* crp = P->c_row_ptr;
   const uint32_t* c = P->num_count;
+  // bits that cover every column index plus one, so the empty key
+  // (0xFFFFFFFF) still sorts last once truncated to them
+  int key_bits = 1;
+  while (key_bits < 32 && (uint64_t(1) << key_bits) <= P->ncols) ++key_bits;
   int rc = 0;
-  rc |= launch_num_hash<T, 64, 32>(L(0), c[0], td, nt, crp, cci, cv, ident, s);
-  rc |= launch_num_hash<T, 512, 128>(L(1), c[1], td, nt, crp, cci, cv, ident, s);
-  rc |= launch_num_hash<T, 2048, 256>(L(2), c[2], td, nt, crp, cci, cv, ident, s);
-  rc |= launch_num_hash<T, 8192, 512>(L(3), c[3], td, nt, crp, cci, cv, ident, s);
-  rc |= launch_num_hash<T, 16384, 1024>(L(4), c[4], td, nt, crp, cci, cv, ident, s);
+  rc |= launch_num_hash<T, 64, 32>(L(0), c[0], td, nt, crp, cci, cv, ident, key_bits, s);
+  rc |= launch_num_hash<T, 512, 128>(L(1), c[1], td, nt, crp, cci, cv, ident, key_bits, s);
+  rc |= launch_num_hash<T, 2048, 256>(L(2), c[2], td, nt, crp, cci, cv, ident, key_bits, s);
+  rc |= launch_num_hash<T, 8192, 512>(L(3), c[3], td, nt, crp, cci, cv, ident, key_bits, s);
+  rc |= launch_num_hash<T, 16384, 1024>(L(4), c[4], td, nt, crp, cci, cv, ident, key_bits, s);
   if (rc) return rc;
   if (c[5]) {
     const uint32_t nwords = uint32_t(ceil_div(P->ncols, 32));
-    const uint32_t blocks = dense_clusters(c[5]);
+    const int cl = dense_cl();
+    const uint32_t blocks = dense_rows_in_flight(c[5], cl);
     RDMM_CUDA_TRY(P->bitmaps.ensure(size_t(blocks) * nwords * 4));
     RDMM_CUDA_TRY(cudaMemsetAsync(P->bitmaps.p, 0, size_t(blocks) * nwords * 4, s));
     RDMM_CUDA_TRY(P->dense.ensure(size_t(blocks) * P->ncols * sizeof(T)));
@@ -685,10 +860,16 @@ int numeric_impl(rdmm_spgemm_plan* P, uint32_t* cci, T* cv, cudaStream_t s) {
     count_launch();
     k_fill<T><<<unsigned(std::min<uint64_t>(ceil_div(nd, 256), 4096)), 256, 0, s>>>(
         P->dense.as<T>(), nd, ident);
-    count_launch();
-    k_dense_cluster<T, true><<<blocks * kCluster, kDenseThreads, 0, s>>>(
-        L(5), c[5], td, nt, nullptr, crp, cci, cv, P->bitmaps.as<uint32_t>(),
-        P->dense.as<T>(), nwords, P->ncols, ident);
+    auto* bm = P->bitmaps.as<uint32_t>();
+    T* dn = P->dense.as<T>();
+    int rc2 = 0;
+    switch (cl) {
+      case 8: rc2 = launch_dense_num<T, 8>(blocks, L(5), c[5], td, nt, crp, cci, cv, bm, dn, nwords, P->ncols, ident, s); break;
+      case 4: rc2 = launch_dense_num<T, 4>(blocks, L(5), c[5], td, nt, crp, cci, cv, bm, dn, nwords, P->ncols, ident, s); break;
+      case 2: rc2 = launch_dense_num<T, 2>(blocks, L(5), c[5], td, nt, crp, cci, cv, bm, dn, nwords, P->ncols, ident, s); break;
+      default: rc2 = launch_dense_num<T, 1>(blocks, L(5), c[5], td, nt, crp, cci, cv, bm, dn, nwords, P->ncols, ident, s);
+    }
+    if (rc2) return rc2;
   }
   RDMM_CUDA_TRY(cudaGetLastError());
   return RDMM_OK;
