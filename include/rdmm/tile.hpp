@@ -284,6 +284,49 @@ FlopMeter spmm_local(DevCsrView<T> a, DevDenseConstView<T> b, DevDenseView<T> c,
   return m;
 }
 
+// Fused stationary-C product of one tile column: c += sum_k a_k * b_k in ONE
+// pass over c (the K A tiles are concatenated side by side on the device,
+// B is read as K row segments).  col_stride = rows of each b_k but the last.
+template <typename T>
+FlopMeter spmm_fused(rdmm_fabric* f, std::uint32_t rank, const std::vector<DevCsrView<T>>& a,
+                     const std::vector<DevDenseConstView<T>>& b, std::uint64_t col_stride,
+                     DevDenseView<T> c, rdmm_stream_t stream, bool c_zero = false) {
+  const std::size_t K = a.size();
+  if (K == 0 || b.size() != K || K > 16) throw std::invalid_argument("spmm_fused: 1..16 tiles");
+  if (K == 1) return spmm_local<T>(a[0], b[0], c, stream, c_zero);
+  std::uint64_t nnz = 0;
+  std::vector<const index_t*> rp(K), ci(K);
+  std::vector<const void*> vv(K), bs(K);
+  for (std::size_t k = 0; k < K; ++k) {
+    if (a[k].rows != c.rows || a[k].cols != b[k].rows || b[k].cols != c.cols ||
+        b[k].ld != b[0].ld || (k + 1 < K && b[k].rows != col_stride))
+      throw dimension_error("spmm_fused: dimension mismatch");
+    nnz += a[k].nnz;
+    rp[k] = a[k].row_ptr;
+    ci[k] = a[k].col_idx;
+    vv[k] = a[k].values;
+    bs[k] = b[k].values;
+  }
+  DevBuffer crp(f, rank, (std::uint64_t(c.rows) + 1) * sizeof(index_t), stream);
+  DevBuffer cci(f, rank, nnz * sizeof(index_t), stream);
+  DevBuffer cvv(f, rank, nnz * sizeof(T), stream);
+  check(rdmm_csr_concat_cols(dtype_bytes<T>(), c.rows, std::uint32_t(K), rp.data(), ci.data(),
+                             vv.data(), col_stride, static_cast<index_t*>(crp.get()),
+                             static_cast<index_t*>(cci.get()), cvv.get(), stream),
+        "spmm_fused concat");
+  std::uint64_t fl = 0;
+  check(rdmm_spmm_csr_seg(dtype_bytes<T>(), c.rows, c.cols, nnz,
+                          static_cast<const index_t*>(crp.get()),
+                          static_cast<const index_t*>(cci.get()), cvv.get(), bs.data(),
+                          std::uint32_t(K), std::uint32_t(col_stride), b[0].ld, c.values, c.ld,
+                          c_zero ? RDMM_SPMM_C_ZERO : 0u, nullptr, 0, stream, &fl),
+        "spmm_fused");
+  FlopMeter m;
+  m.flops = fl;
+  m.output_nnz = std::uint64_t(c.rows) * c.cols;
+  return m;  // the concat buffers are released stream-ordered after the kernel
+}
+
 // c += x (tile.hpp:300-307); x may live in a peer GPU's heap (NVLink loads).
 template <typename T>
 void dense_add_into(DevDenseView<T> c, DevDenseConstView<T> x, rdmm_stream_t stream) {

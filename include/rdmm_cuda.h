@@ -102,6 +102,18 @@ int rdmm_spmm_csr_ex(int dtype_bytes, uint32_t rows, uint32_t cols, uint32_t n,
                      void* workspace, size_t workspace_bytes,
                      rdmm_stream_t stream, uint64_t* flops);
 
+/* Fused K-tile form: C += A * [B_0; B_1; ...] where B is given as nseg
+ * (<= 16) row segments of seg_rows rows each (the B(k,j) tiles of one tile
+ * column, stacked), all with leading dimension ldb.  A's column g reads row
+ * g % seg_rows of segment g / seg_rows.  One pass over A and C for the whole
+ * tile column (stationary-C with K tiles, algos.hpp:378-415). */
+int rdmm_spmm_csr_seg(int dtype_bytes, uint32_t rows, uint32_t n, uint64_t nnz,
+                      const uint32_t* row_ptr, const uint32_t* col_idx,
+                      const void* val, const void* const* bseg, uint32_t nseg,
+                      uint32_t seg_rows, uint64_t ldb, void* C, uint64_t ldc,
+                      unsigned flags, void* workspace, size_t workspace_bytes,
+                      rdmm_stream_t stream, uint64_t* flops);
+
 /* ---------------------------------------------------------------- SpGEMM */
 /*
  * C = sum_t A_t * B_t  over a list of terms, rows x ncols, sorted rows,
@@ -166,6 +178,16 @@ int rdmm_csr_extract_fill(int dtype_bytes, const uint32_t* row_ptr,
                           uint32_t ncols, const uint32_t* out_rp,
                           uint32_t* out_ci, void* out_val,
                           rdmm_stream_t stream);
+/* Concatenate K (<= 16) CSR tiles of the same rows side by side: tile k's
+ * columns are offset by k*col_stride (the A(i,0..K-1) tiles of one tile row
+ * -> one CSR for the fused K-tile SpMM).  out_rp has rows+1 entries, out_ci
+ * / out_val the sum of the tiles' nnz. */
+int rdmm_csr_concat_cols(int dtype_bytes, uint32_t rows, uint32_t K,
+                         const uint32_t* const* row_ptr,
+                         const uint32_t* const* col_idx,
+                         const void* const* values, uint64_t col_stride,
+                         uint32_t* out_rp, uint32_t* out_ci, void* out_val,
+                         rdmm_stream_t stream);
 /* Sum of a dense tile's values in double (checksum, algos.hpp:634-669). */
 int rdmm_tile_sum(int dtype_bytes, uint32_t rows, uint32_t cols, uint64_t ld,
                   const void* p, rdmm_stream_t stream, double* out);

@@ -82,6 +82,7 @@ typedef struct {
   int lookahead;
   int ws_local_inplace;
   int checksum;
+  int fuse_k;
 } rdmm_h_options;
 
 #define RDMM_H_MAX_RANKS 64

@@ -94,6 +94,7 @@ RunOptions opts_of(const rdmm_h_options* o) {
   r.lookahead = o->lookahead > 0 ? o->lookahead : 2;
   r.ws_local_inplace = o->ws_local_inplace != 0;
   r.checksum = o->checksum != 0;
+  r.fuse_k = o->fuse_k != 0;
   return r;
 }
 

@@ -94,7 +94,21 @@ struct SpmmArgs {
   uint64_t nnz, Q;
   uint32_t rows, nvec, nchunks, wstride;
   int prefetch;
+  // Segmented B (fused K-tile products): B row g lives in segment
+  // g / seg_rows at row g % seg_rows; nseg == 0 means one contiguous B.
+  const T* bseg[16];
+  uint64_t boff;  // element offset applied to every segment (column panel)
+  uint32_t nseg, seg_rows, seg_shift;
 };
+
+template <typename T, typename V>
+__device__ __forceinline__ const V* brow_ptr(const SpmmArgs<T>& p, const V* Bv, uint32_t k,
+                                             uint64_t ldbv, uint32_t voff) {
+  if (p.nseg == 0) return Bv + uint64_t(k) * ldbv + voff;
+  const uint32_t sg = p.seg_shift < 32 ? (k >> p.seg_shift) : (k / p.seg_rows);
+  const uint32_t r = k - sg * p.seg_rows;
+  return reinterpret_cast<const V*>(p.bseg[sg] + p.boff) + uint64_t(r) * ldbv + voff;
+}
 
 template <int G>
 __device__ __forceinline__ unsigned group_mask() {
@@ -224,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
             const int q = t + u;
             const uint32_t k = __shfl_sync(gm, kk[q / G], q % G, G);
             if (q < int(cnt)) {
-              const V* brow = Bv + uint64_t(k) * ldbv + lane;
+              const V* brow = brow_ptr<T, V>(p, Bv, k, ldbv, lane);
 #pragma unroll
               for (int v = 0; v < NV; ++v)
                 if (colok[v]) bv[u][v] = __ldg(brow + G * v);
@@ -376,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
                 const int q = t + u;
                 const uint32_t k = __shfl_sync(gm, kk[q / G], q % G, G);
                 if (q < int(cnt)) {
-                  const V* brow = Bv + uint64_t(k) * ldbv + lane;
+                  const V* brow = brow_ptr<T, V>(p, Bv, k, ldbv, lane);
 #pragma unroll
                   for (int v = 0; v < NV; ++v)
                     if (colok[v]) bv[u][v] = __ldg(brow + G * v);
@@ -414,6 +428,85 @@ __global__ void __launch_bounds__(kThreads, MINB)
       if (r >= p.rows) break;
     }
     if (lane == 0) p.tail_row[c] = trow;
+  }
+}
+
+// Narrow rows (N < 128 fp32: L = N/4 < 32 vectors per B row): a warp owns a
+// chunk and walks it S = 32/L rows at a time in lock-step; lane (s, v)
+// accumulates vector v of the group's s-th row.  Every lane loads its own
+// row's col/val (broadcast within the L lanes), so no shuffles are needed and
+// the warp never diverges into per-group code paths; U gathers per lane are
+// in flight, i.e. 8*S nonzeros per warp.  Rows keep the reference order
+// (fma chain from C) exactly like the wide kernels.
+template <typename T, int VEC, int L, bool CZERO>
+__global__ void __launch_bounds__(kThreads)
+    spmm_lockstep(const SpmmArgs<T> p) {
+  using V = typename VecOf<T, VEC>::type;
+  constexpr int S = 32 / L;
+  constexpr int U = 8;
+  const uint32_t lane = threadIdx.x & 31u, sl = lane / L, v = lane % L;
+  const uint32_t warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = gridDim.x * (kThreads / 32);
+  const V* __restrict__ Bv = reinterpret_cast<const V*>(p.B);
+  V* __restrict__ Cv = reinterpret_cast<V*>(p.C);
+  const uint64_t ldbv = p.ldb / VEC, ldcv = p.ldc / VEC;
+  const bool colok = v < p.nvec;
+  for (uint32_t c = warp; c < p.nchunks; c += nwarps) {
+    const uint64_t lo = uint64_t(c) * p.Q;
+    const uint64_t hi = umin(lo + p.Q, p.nnz);
+    uint32_t l = 0, h = p.rows;
+    while (h - l > 1) {
+      const uint32_t m = (l + h) >> 1;
+      if (__ldg(p.rp + m) <= lo)
+        l = m;
+      else
+        h = m;
+    }
+    uint32_t trow1 = 0;  // tail row + 1 (0: none)
+    for (uint32_t rb = l;; rb += S) {
+      const uint32_t r = rb + sl;
+      uint32_t rs = 0, re = 0;
+      if (r < p.rows) {
+        rs = __ldg(p.rp + r);
+        re = __ldg(p.rp + r + 1);
+      }
+      const bool live = r < p.rows && rs < hi;
+      if (!__any_sync(0xffffffffu, live)) break;
+      const uint64_t s0 = umax(rs, lo), e0 = live ? umin(re, hi) : s0;
+      const uint32_t len = e0 > s0 ? uint32_t(e0 - s0) : 0u;
+      const bool starts = rs >= lo, ends = re <= hi;
+      V acc = (!CZERO && len && starts && colok) ? Cv[uint64_t(r) * ldcv + v] : vzero<V>();
+      const uint32_t maxlen = __reduce_max_sync(0xffffffffu, len);
+      for (uint32_t j = 0; j < maxlen; j += U) {
+        uint32_t kk[U];
+        T aa[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool ok = j + u < len;
+          kk[u] = ok ? __ldg(p.ci + s0 + j + u) : 0u;
+          aa[u] = ok ? __ldg(p.val + s0 + j + u) : T(0);
+        }
+        V bv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j + u < len && colok) bv[u] = __ldg(brow_ptr<T, V>(p, Bv, kk[u], ldbv, v));
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j + u < len && colok) acc = vfma(aa[u], bv[u], acc);
+      }
+      if (len && colok) {
+        if (starts && ends) {
+          __stcs(Cv + uint64_t(r) * ldcv + v, acc);
+        } else {
+          V* dst = reinterpret_cast<V*>(starts ? p.tail_val : p.head_val) +
+                   uint64_t(c) * (p.wstride / VEC);
+          dst[v] = acc;
+        }
+      }
+      if (len && starts && !ends) trow1 = r + 1;
+    }
+    trow1 = __reduce_max_sync(0xffffffffu, trow1);
+    if (lane == 0) p.tail_row[c] = int32_t(trow1) - 1;
   }
 }
 
@@ -484,6 +577,14 @@ void launch(const SpmmArgs<T>& a, bool czero, int blocks, int fix_blocks,
   // wider rows (NV>=2) keep more gathers in flight per lane and the
   // row-oriented kernel is faster there (at the HBM gather roofline on ER).
   const int kv = kernel_variant();
+  if constexpr (G < 32 && NV == 1) {
+    if (kv != 1) {  // narrow rows: lock-step warp kernel
+      if (czero) spmm_lockstep<T, VEC, G, true><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_lockstep<T, VEC, G, false><<<blocks, kThreads, 0, s>>>(a);
+      spmm_fixup<T, VEC, G, NV><<<fix_blocks, kThreads, 0, s>>>(a);
+      return;
+    }
+  }
   const bool use_rows = kv == 1 || (kv == 0 && !(G == 32 && NV == 1));
   const int ov = occ_variant();
   const bool occ4 = G == 32 && NV == 1 && (ov == 4 || (ov == 0 && !use_rows));
@@ -601,19 +702,24 @@ template <typename T>
 int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
               const uint32_t* rp, const uint32_t* ci, const T* val, const T* B,
               uint64_t ldb, T* C, uint64_t ldc, unsigned flags, void* ws,
-              size_t ws_bytes, rdmm_stream_t stream, uint64_t* flops) {
+              size_t ws_bytes, rdmm_stream_t stream, uint64_t* flops,
+              const T* const* bseg = nullptr, uint32_t nseg = 0, uint32_t seg_rows = 0) {
   if (flops) *flops = 2ull * nnz * n;
   const bool czero = (flags & RDMM_SPMM_C_ZERO) != 0;
   if (ldb < n || ldc < n)
     return fail(RDMM_ERR_DIMENSION, "spmm: leading dimension smaller than n");
   if (rows == 0 || n == 0 || nnz == 0) return RDMM_OK;
-  if (!rp || !ci || !val || !B || !C)
+  if (!rp || !ci || !val || (!B && !nseg) || !C)
     return fail(RDMM_ERR_INVALID, "spmm: null device pointer");
   (void)cols;
   cudaStream_t s = as_stream(stream);
   constexpr int VV = sizeof(T) == 4 ? 4 : 2;
+  if (nseg > 16) return fail(RDMM_ERR_INVALID, "spmm: at most 16 B segments");
+  bool seg_aligned = true;
+  for (uint32_t q = 0; q < nseg; ++q)
+    seg_aligned &= (reinterpret_cast<uintptr_t>(bseg[q]) % 16) == 0;
   const bool vec_ok = n % VV == 0 && ldb % VV == 0 && ldc % VV == 0 &&
-                      (reinterpret_cast<uintptr_t>(B) % 16) == 0 &&
+                      (nseg ? seg_aligned : (reinterpret_cast<uintptr_t>(B) % 16) == 0) &&
                       (reinterpret_cast<uintptr_t>(C) % 16) == 0;
   const SpmmPlan P = make_plan<T>(nnz, n, vec_ok);
   void* w = ws;
@@ -634,6 +740,14 @@ int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
   a.nchunks = P.nchunks;
   a.wstride = P.wstride;
   a.prefetch = (flags & RDMM_SPMM_NO_PREFETCH) ? 0 : prefetch_default();
+  a.nseg = nseg;
+  a.seg_rows = seg_rows;
+  a.seg_shift = 32;
+  if (nseg) {
+    if (seg_rows == 0) return fail(RDMM_ERR_INVALID, "spmm: seg_rows must be positive");
+    for (uint32_t q = 0; q < nseg; ++q) a.bseg[q] = bseg[q];
+    if ((seg_rows & (seg_rows - 1)) == 0) a.seg_shift = uint32_t(__builtin_ctz(seg_rows));
+  }
   char* base = static_cast<char*>(w);
   const size_t vbytes = size_t(P.nchunks) * P.wstride * sizeof(T);
   a.head_val = reinterpret_cast<T*>(base);
@@ -646,7 +760,8 @@ int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
     const uint32_t nv = std::min<uint32_t>(P.pv, nvec_total - v0);
     int nvp = 1;
     const int g = groups_for(nv, &nvp);
-    a.B = B + uint64_t(v0) * P.VEC;
+    a.B = nseg ? nullptr : B + uint64_t(v0) * P.VEC;
+    a.boff = uint64_t(v0) * P.VEC;
     a.C = C + uint64_t(v0) * P.VEC;
     a.nvec = nv;
     if (P.VEC == 1)
@@ -710,4 +825,26 @@ extern "C" int rdmm_spmm_csr_ex(int dtype_bytes, uint32_t rows, uint32_t cols,
                           static_cast<const float*>(B), ldb,
                           static_cast<float*>(C), ldc, flags, workspace,
                           workspace_bytes, stream, flops);
+}
+
+extern "C" int rdmm_spmm_csr_seg(int dtype_bytes, uint32_t rows, uint32_t n,
+                                 uint64_t nnz, const uint32_t* row_ptr,
+                                 const uint32_t* col_idx, const void* val,
+                                 const void* const* bseg, uint32_t nseg,
+                                 uint32_t seg_rows, uint64_t ldb, void* C,
+                                 uint64_t ldc, unsigned flags, void* workspace,
+                                 size_t workspace_bytes, rdmm_stream_t stream,
+                                 uint64_t* flops) {
+  if (dtype_bytes == 8)
+    return spmm_impl<double>(rows, nseg * seg_rows, n, nnz, row_ptr, col_idx,
+                             static_cast<const double*>(val), nullptr, ldb,
+                             static_cast<double*>(C), ldc, flags, workspace,
+                             workspace_bytes, stream, flops,
+                             reinterpret_cast<const double* const*>(bseg), nseg,
+                             seg_rows);
+  return spmm_impl<float>(rows, nseg * seg_rows, n, nnz, row_ptr, col_idx,
+                          static_cast<const float*>(val), nullptr, ldb,
+                          static_cast<float*>(C), ldc, flags, workspace,
+                          workspace_bytes, stream, flops,
+                          reinterpret_cast<const float* const*>(bseg), nseg, seg_rows);
 }

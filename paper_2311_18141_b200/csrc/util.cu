@@ -74,6 +74,44 @@ __global__ void k_tile_sum(uint32_t rows, uint32_t cols, uint64_t ld,
   if (threadIdx.x == 0) atomicAdd(out, s);
 }
 
+struct ConcatArgs {
+  const uint32_t* rp[16];
+  const uint32_t* ci[16];
+  const void* val[16];
+  uint32_t K;
+  uint64_t col_stride;
+};
+
+__global__ void k_concat_rowptr(ConcatArgs a, uint32_t rows, uint32_t* out_rp) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r <= rows;
+       r += gridDim.x * blockDim.x) {
+    uint32_t s = 0;
+    for (uint32_t k = 0; k < a.K; ++k) s += a.rp[k][r];
+    out_rp[r] = s;
+  }
+}
+
+template <typename T>
+__global__ void k_concat_fill(ConcatArgs a, uint32_t rows, const uint32_t* out_rp,
+                              uint32_t* out_ci, T* out_val) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = w; r < rows; r += nw) {
+    uint32_t o = out_rp[r];
+    for (uint32_t k = 0; k < a.K; ++k) {
+      const uint32_t s = a.rp[k][r], e = a.rp[k][r + 1];
+      const uint32_t off = uint32_t(k * a.col_stride);
+      const T* v = static_cast<const T*>(a.val[k]);
+      for (uint32_t q = lane; q < e - s; q += 32) {
+        out_ci[o + q] = a.ci[k][s + q] + off;
+        out_val[o + q] = v[s + q];
+      }
+      o += e - s;
+    }
+  }
+}
+
 __global__ void k_spin(unsigned long long ns) {
   const unsigned long long t0 = clock64();
   // clock64 runs at the SM clock (~1.9 GHz); spin ~ns nanoseconds
@@ -162,6 +200,36 @@ extern "C" int rdmm_spin_delay(uint64_t ns, rdmm_stream_t stream) {
   count_launch();
   if (!ns) return RDMM_OK;
   k_spin<<<1, 1, 0, as_stream(stream)>>>(ns);
+  RDMM_CUDA_TRY(cudaGetLastError());
+  return RDMM_OK;
+}
+
+extern "C" int rdmm_csr_concat_cols(int dtype_bytes, uint32_t rows, uint32_t K,
+                                    const uint32_t* const* rp,
+                                    const uint32_t* const* ci,
+                                    const void* const* val, uint64_t col_stride,
+                                    uint32_t* out_rp, uint32_t* out_ci,
+                                    void* out_val, rdmm_stream_t stream) {
+  if (K == 0 || K > 16) return fail(RDMM_ERR_INVALID, "concat: 1..16 tiles");
+  ConcatArgs a{};
+  for (uint32_t k = 0; k < K; ++k) {
+    a.rp[k] = rp[k];
+    a.ci[k] = ci[k];
+    a.val[k] = val[k];
+  }
+  a.K = K;
+  a.col_stride = col_stride;
+  cudaStream_t s = as_stream(stream);
+  const unsigned b1 = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>(ceil_div(uint64_t(rows) + 1, 256), uint64_t(num_sms()) * 8)));
+  count_launch(2);
+  k_concat_rowptr<<<b1, 256, 0, s>>>(a, rows, out_rp);
+  const unsigned b2 = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>(ceil_div(rows, 8), uint64_t(num_sms()) * 16)));
+  if (dtype_bytes == 8)
+    k_concat_fill<double><<<b2, 256, 0, s>>>(a, rows, out_rp, out_ci, static_cast<double*>(out_val));
+  else
+    k_concat_fill<float><<<b2, 256, 0, s>>>(a, rows, out_rp, out_ci, static_cast<float*>(out_val));
   RDMM_CUDA_TRY(cudaGetLastError());
   return RDMM_OK;
 }

@@ -116,8 +116,9 @@ def test_offset_and_prefetch_toggles(dist, orc):
     base, want, _ = run_spmm(dist, orc, variant="stationary_c")
     no_off, _, _ = run_spmm(dist, orc, variant="stationary_c", offset=False)
     no_pre, _, _ = run_spmm(dist, orc, variant="stationary_c", prefetch=False)
+    no_fuse, _, _ = run_spmm(dist, orc, variant="stationary_c", fuse_k=False)
     assert np.array_equal(base, want) and np.array_equal(no_off, base)
-    assert np.array_equal(no_pre, base)
+    assert np.array_equal(no_pre, base) and np.array_equal(no_fuse, base)
     a_off, want2, _ = run_spmm(dist, orc, variant="stationary_a", offset=False)
     assert np.array_equal(a_off, want2)
     wl, want3, _ = run_spmm(dist, orc, variant="ws_locality", ws_base="stationary_c")
