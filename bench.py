@@ -281,6 +281,18 @@ def run_ours(args, cfg, dev, rank, world):
     kms, kcount = L.kernel_time(kind_id)
     L.rdmm_kernel_timing(0)
     ms_local = sum(per) / len(per)
+    imbalance = None
+    if tdist:  # per-rank work and time, for the reference's imbalance metrics
+        tt = torch.tensor([ms_local, float(flops_local)], device=dev, dtype=torch.float64)
+        allt = [torch.zeros_like(tt) for _ in range(world)]
+        tdist.all_gather(allt, tt)
+        times = [float(x[0]) for x in allt]
+        works = [float(x[1]) for x in allt]
+        imbalance = {"time_max_over_avg": max(times) / (sum(times) / world),
+                     "flops_max_over_avg": max(works) / max(1e-30, sum(works) / world),
+                     "per_rank_ms": times,
+                     "definition": "max/avg over ranks (analytics.hpp:58-89 applied to "
+                                   "per-rank device time and FlopMeter work)"}
     if tdist:  # max over ranks of the device time; flops summed over ranks
         t = torch.tensor([ms_local, float(flops_local), float(steals)], device=dev,
                          dtype=torch.float64)
@@ -382,6 +394,8 @@ def run_ours(args, cfg, dev, rank, world):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if imbalance:
+        out["imbalance"] = imbalance
     if out_nnz is not None:
         out["config"]["nnz_out"] = out_nnz
     f.close()

@@ -172,6 +172,47 @@ __device__ __forceinline__ void enumerate_row(uint32_t r,
   }
 }
 
+// Heavy rows: each warp of the CTA (and of the `nparts` CTAs sharing the
+// row) takes whole A entries, its lanes stride over the entry's B row
+// (coalesced, no search); two products per lane are loaded before they are
+// inserted.  Used by the large CTA tiers and the dense tier.
+template <typename T, int G, bool kValues, class Ins>
+__device__ __forceinline__ void enumerate_row_warps(uint32_t r, const TermDev<T>* terms,
+                                                    int nterms, Ins ins, uint32_t part = 0,
+                                                    uint32_t nparts = 1) {
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr uint32_t W = G / 32;
+  const uint32_t gw = part * W + wid, nw = nparts * W;
+  for (int t = 0; t < nterms; ++t) {
+    const TermDev<T> tm = terms[t];
+    const bool ident = tm.arp == nullptr;
+    const uint32_t s0 = ident ? 0u : __ldg(tm.arp + r);
+    const uint32_t s1 = ident ? 1u : __ldg(tm.arp + r + 1);
+    for (uint32_t e = s0 + gw; e < s1; e += nw) {
+      const uint32_t k = ident ? r : __ldg(tm.aci + e);
+      T a = T(1);
+      if (kValues && !ident) a = __ldg(tm.av + e);
+      const uint32_t bs = __ldg(tm.brp + k), be = __ldg(tm.brp + k + 1);
+      for (uint32_t q = bs + lane; q < be; q += 64) {
+        const bool two = q + 32 < be;
+        const uint32_t k0 = __ldg(tm.bci + q);
+        const uint32_t k1 = two ? __ldg(tm.bci + q + 32) : 0u;
+        T v0 = T(0), v1 = T(0);
+        if (kValues) {
+          v0 = __ldg(tm.bv + q);
+          if (two) v1 = __ldg(tm.bv + q + 32);
+          if (!ident) {
+            v0 = a * v0;
+            v1 = a * v1;
+          }
+        }
+        ins(k0, v0);
+        if (two) ins(k1, v1);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------ binning
 
 // Warp per row: ub[r] = number of products; bin by symbolic tier.  Per-term
@@ -265,15 +306,20 @@ __global__ void __launch_bounds__(G == 32 ? 256 : G)
     const uint32_t r = active ? list[li] : 0u;
     for (uint32_t i = tg; i < TAB; i += G) keys[i] = kEmpty;
     gsync<G>();
-    if (active)
-      enumerate_row<T, G, false>(r, terms, nterms, *win, [&](uint32_t key, T) {
+    auto sym_ins = [&](uint32_t key, T) {
         uint32_t s = hslot(key, LOG2T);
         for (;;) {
           const uint32_t old = atomicCAS(keys + s, kEmpty, key);
           if (old == kEmpty || old == key) break;
           s = (s + 1) & (TAB - 1);
         }
-      });
+    };
+    if (active) {
+      if constexpr (G >= 512)
+        enumerate_row_warps<T, G, false>(r, terms, nterms, sym_ins);
+      else
+        enumerate_row<T, G, false>(r, terms, nterms, *win, sym_ins);
+    }
     gsync<G>();
     uint32_t c = 0;
     for (uint32_t i = tg; i < TAB; i += G) c += keys[i] != kEmpty;
@@ -323,8 +369,7 @@ __global__ void __launch_bounds__(G == 32 ? 256 : G)
       vals[i] = ident_val;
     }
     gsync<G>();
-    if (active)
-      enumerate_row<T, G, true>(r, terms, nterms, *win, [&](uint32_t key, T v) {
+    auto num_ins = [&](uint32_t key, T v) {
         uint32_t s = hslot(key, LOG2T);
         for (;;) {
           const uint32_t old = atomicCAS(keys + s, kEmpty, key);
@@ -332,7 +377,13 @@ __global__ void __launch_bounds__(G == 32 ? 256 : G)
           s = (s + 1) & (TAB - 1);
         }
         atomicAdd(vals + s, v);
-      });
+    };
+    if (active) {
+      if constexpr (G >= 512)
+        enumerate_row_warps<T, G, true>(r, terms, nterms, num_ins);
+      else
+        enumerate_row<T, G, true>(r, terms, nterms, *win, num_ins);
+    }
     gsync<G>();
     if constexpr (G == 32) {
       // warp tier: bitonic sort of the 64-slot table; empty keys sort last
@@ -444,14 +495,18 @@ __global__ void __launch_bounds__(kDenseThreads)
   __syncthreads();
   for (uint32_t li = cid; li < count; li += ncl) {
     const uint32_t r = list[li];
-    enumerate_row<T, G, true>(
-        r, terms, nterms, win,
+    enumerate_row_warps<T, G, true>(
+        r, terms, nterms,
         [&](uint32_t key, T v) {
-          const uint32_t bit = 1u << (key & 31);
-          if (!(__ldcg(bm + (key >> 5)) & bit)) atomicOr(bm + (key >> 5), bit);
           const uint32_t sl = hslot(key, LOG2W);
           const uint32_t old = atomicCAS(wkey + sl, kEmpty, key);
-          if (old == kEmpty || old == key)
+          if (old == key) {  // cached: its bit is already set
+            atomicAdd(wval + sl, v);
+            return;
+          }
+          const uint32_t bit = 1u << (key & 31);
+          if (!(__ldcg(bm + (key >> 5)) & bit)) atomicOr(bm + (key >> 5), bit);
+          if (old == kEmpty)
             atomicAdd(wval + sl, v);
           else
             atomicAdd(dv + key, v);
@@ -511,7 +566,7 @@ __global__ void __launch_bounds__(kDenseThreads)
   __syncthreads();
   for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
     const uint32_t r = list[li];
-    enumerate_row<T, G, false>(r, terms, nterms, win, [&](uint32_t key, T) {
+    enumerate_row_warps<T, G, false>(r, terms, nterms, [&](uint32_t key, T) {
       const uint32_t bit = 1u << (key & 31);
       if (!(bm[key >> 5] & bit)) atomicOr(bm + (key >> 5), bit);
     });
@@ -538,7 +593,7 @@ __global__ void __launch_bounds__(kDenseThreads)
   uint32_t* bm = bitmaps + size_t(blockIdx.x) * nwords;
   for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
     const uint32_t r = list[li];
-    enumerate_row<T, G, false>(r, terms, nterms, win, [&](uint32_t key, T) {
+    enumerate_row_warps<T, G, false>(r, terms, nterms, [&](uint32_t key, T) {
       const uint32_t bit = 1u << (key & 31);
       if (!(__ldcg(bm + (key >> 5)) & bit)) atomicOr(bm + (key >> 5), bit);
     });

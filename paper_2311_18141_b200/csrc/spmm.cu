@@ -101,10 +101,10 @@ struct SpmmArgs {
   uint32_t nseg, seg_rows, seg_shift;
 };
 
-template <typename T, typename V>
+template <typename T, typename V, bool SEG>
 __device__ __forceinline__ const V* brow_ptr(const SpmmArgs<T>& p, const V* Bv, uint32_t k,
                                              uint64_t ldbv, uint32_t voff) {
-  if (p.nseg == 0) return Bv + uint64_t(k) * ldbv + voff;
+  if constexpr (!SEG) return Bv + uint64_t(k) * ldbv + voff;
   const uint32_t sg = p.seg_shift < 32 ? (k >> p.seg_shift) : (k / p.seg_rows);
   const uint32_t r = k - sg * p.seg_rows;
   return reinterpret_cast<const V*>(p.bseg[sg] + p.boff) + uint64_t(r) * ldbv + voff;
@@ -167,7 +167,7 @@ __device__ __forceinline__ void win_load(uint32_t (&rew)[SL],
 // is flushed to C (or to a carry slot if the chunk cuts it) when the stream
 // crosses its end.  CZERO: C is known to be zero on entry (first product
 // into a fresh tile), so C is written but never read.
-template <typename T, int VEC, int G, int NV, bool CZERO, int MINB>
+template <typename T, int VEC, int G, int NV, bool CZERO, int MINB, bool SEG>
 __global__ void __launch_bounds__(kThreads, MINB)
     spmm_stream(const SpmmArgs<T> p) {
   using V = typename VecOf<T, VEC>::type;
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
             const int q = t + u;
             const uint32_t k = __shfl_sync(gm, kk[q / G], q % G, G);
             if (q < int(cnt)) {
-              const V* brow = brow_ptr<T, V>(p, Bv, k, ldbv, lane);
+              const V* brow = brow_ptr<T, V, SEG>(p, Bv, k, ldbv, lane);
 #pragma unroll
               for (int v = 0; v < NV; ++v)
                 if (colok[v]) bv[u][v] = __ldg(brow + G * v);
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
 
 // Row-oriented variant: the worker walks the chunk row by row; each row
 // (or the chunk's slice of it) is accumulated from its own col/val window.
-template <typename T, int VEC, int G, int NV, bool CZERO, int MINB>
+template <typename T, int VEC, int G, int NV, bool CZERO, int MINB, bool SEG>
 __global__ void __launch_bounds__(kThreads, MINB)
     spmm_rows(const SpmmArgs<T> p) {
   using V = typename VecOf<T, VEC>::type;
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
                 const int q = t + u;
                 const uint32_t k = __shfl_sync(gm, kk[q / G], q % G, G);
                 if (q < int(cnt)) {
-                  const V* brow = brow_ptr<T, V>(p, Bv, k, ldbv, lane);
+                  const V* brow = brow_ptr<T, V, SEG>(p, Bv, k, ldbv, lane);
 #pragma unroll
                   for (int v = 0; v < NV; ++v)
                     if (colok[v]) bv[u][v] = __ldg(brow + G * v);
@@ -431,19 +431,19 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
-// Narrow rows (N < 128 fp32: L = N/4 < 32 vectors per B row): a warp owns a
-// chunk and walks it S = 32/L rows at a time in lock-step; lane (s, v)
-// accumulates vector v of the group's s-th row.  Every lane loads its own
-// row's col/val (broadcast within the L lanes), so no shuffles are needed and
-// the warp never diverges into per-group code paths; U gathers per lane are
-// in flight, i.e. 8*S nonzeros per warp.  Rows keep the reference order
-// (fma chain from C) exactly like the wide kernels.
-template <typename T, int VEC, int L, bool CZERO>
+// Narrow rows (N < 128 fp32: L = N/4 < 32 vectors per B row): the whole warp
+// works on ONE row at a time; lane (s, v) takes every S-th nonzero of the
+// row (S = 32/L slots) and vector v of its B row, so S gathers of L*16 bytes
+// are in flight per load instruction and the warp never splits into
+// divergent per-row groups; the S partial sums of a row are combined with
+// shuffles before the store.  (Summation order differs from the reference
+// for real values: slot partials, then their sum; exact for integer data.)
+template <typename T, int VEC, int L, bool CZERO, bool SEG>
 __global__ void __launch_bounds__(kThreads)
-    spmm_lockstep(const SpmmArgs<T> p) {
+    spmm_vec(const SpmmArgs<T> p) {
   using V = typename VecOf<T, VEC>::type;
   constexpr int S = 32 / L;
-  constexpr int U = 8;
+  constexpr int U = 4;
   const uint32_t lane = threadIdx.x & 31u, sl = lane / L, v = lane % L;
   const uint32_t warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
   const uint32_t nwarps = gridDim.x * (kThreads / 32);
@@ -462,51 +462,65 @@ __global__ void __launch_bounds__(kThreads)
       else
         h = m;
     }
-    uint32_t trow1 = 0;  // tail row + 1 (0: none)
-    for (uint32_t rb = l;; rb += S) {
-      const uint32_t r = rb + sl;
-      uint32_t rs = 0, re = 0;
-      if (r < p.rows) {
-        rs = __ldg(p.rp + r);
-        re = __ldg(p.rp + r + 1);
-      }
-      const bool live = r < p.rows && rs < hi;
-      if (!__any_sync(0xffffffffu, live)) break;
-      const uint64_t s0 = umax(rs, lo), e0 = live ? umin(re, hi) : s0;
-      const uint32_t len = e0 > s0 ? uint32_t(e0 - s0) : 0u;
-      const bool starts = rs >= lo, ends = re <= hi;
-      V acc = (!CZERO && len && starts && colok) ? Cv[uint64_t(r) * ldcv + v] : vzero<V>();
-      const uint32_t maxlen = __reduce_max_sync(0xffffffffu, len);
-      for (uint32_t j = 0; j < maxlen; j += U) {
-        uint32_t kk[U];
-        T aa[U];
+    uint32_t r = l;
+    uint32_t rs = __ldg(p.rp + r), re = __ldg(p.rp + r + 1);
+    int32_t trow = -1;
+    while (rs < hi) {
+      const uint32_t re_next = (r + 2 <= p.rows) ? __ldg(p.rp + r + 2) : re;
+      const uint64_t s0 = umax(rs, lo), e0 = umin(re, hi);
+      if (s0 < e0) {
+        const bool starts = rs >= lo, ends = re <= hi;
+        V acc = vzero<V>();
+        for (uint64_t base = s0; base < e0; base += 32) {
+          const uint32_t cnt = uint32_t(umin(32, e0 - base));
+          const bool ok0 = lane < cnt;
+          const uint32_t kk = ok0 ? __ldg(p.ci + base + lane) : 0u;
+          const T aa = ok0 ? __ldg(p.val + base + lane) : T(0);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const bool ok = j + u < len;
-          kk[u] = ok ? __ldg(p.ci + s0 + j + u) : 0u;
-          aa[u] = ok ? __ldg(p.val + s0 + j + u) : T(0);
+          for (int t = 0; t < 32; t += S * U) {
+            if (t < int(cnt)) {
+              V bv[U];
+              T av[U];
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                const int q = t + u * S + int(sl);
+                const uint32_t k = __shfl_sync(0xffffffffu, kk, q & 31);
+                av[u] = __shfl_sync(0xffffffffu, aa, q & 31);
+                if (q < int(cnt) && colok) bv[u] = __ldg(brow_ptr<T, V, SEG>(p, Bv, k, ldbv, v));
+              }
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                const int q = t + u * S + int(sl);
+                if (q < int(cnt) && colok) acc = vfma(av[u], bv[u], acc);
+              }
+            }
+          }
         }
-        V bv[U];
+        // combine the S slot partials (lanes v, v+L, v+2L, ...)
+        T* pa = reinterpret_cast<T*>(&acc);
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (j + u < len && colok) bv[u] = __ldg(brow_ptr<T, V>(p, Bv, kk[u], ldbv, v));
+        for (int off = L; off < 32; off <<= 1)
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (j + u < len && colok) acc = vfma(aa[u], bv[u], acc);
-      }
-      if (len && colok) {
-        if (starts && ends) {
-          __stcs(Cv + uint64_t(r) * ldcv + v, acc);
-        } else {
-          V* dst = reinterpret_cast<V*>(starts ? p.tail_val : p.head_val) +
-                   uint64_t(c) * (p.wstride / VEC);
-          dst[v] = acc;
+          for (int x = 0; x < VEC; ++x) pa[x] += __shfl_xor_sync(0xffffffffu, pa[x], off);
+        if (sl == 0 && colok) {
+          if (starts && ends) {
+            if (!CZERO) acc = vadd(Cv[uint64_t(r) * ldcv + v], acc);
+            __stcs(Cv + uint64_t(r) * ldcv + v, acc);
+          } else {
+            if (!CZERO && starts) acc = vadd(Cv[uint64_t(r) * ldcv + v], acc);
+            V* dst = reinterpret_cast<V*>(starts ? p.tail_val : p.head_val) +
+                     uint64_t(c) * (p.wstride / VEC);
+            dst[v] = acc;
+          }
         }
+        if (starts && !ends) trow = int32_t(r);
       }
-      if (len && starts && !ends) trow1 = r + 1;
+      ++r;
+      rs = re;
+      re = re_next;
+      if (r >= p.rows) break;
     }
-    trow1 = __reduce_max_sync(0xffffffffu, trow1);
-    if (lane == 0) p.tail_row[c] = int32_t(trow1) - 1;
+    if (lane == 0) p.tail_row[c] = trow;
   }
 }
 
@@ -569,19 +583,18 @@ inline int kernel_variant() {
   return v;
 }
 
-template <typename T, int VEC, int G, int NV>
-void launch(const SpmmArgs<T>& a, bool czero, int blocks, int fix_blocks,
-            cudaStream_t s) {
+template <typename T, int VEC, int G, int NV, bool SEG>
+void launch_seg(const SpmmArgs<T>& a, bool czero, int blocks, cudaStream_t s) {
   // Measured on B200 (profiles/): the nnz-stream kernel at
   // 64 registers (4 CTAs/SM) wins for one 16-B vector per lane (N=128 fp32);
   // wider rows (NV>=2) keep more gathers in flight per lane and the
-  // row-oriented kernel is faster there (at the HBM gather roofline on ER).
+  // row-oriented kernel is faster there (at the HBM gather roofline on ER);
+  // narrow rows (N<128) use the whole-warp row kernel.
   const int kv = kernel_variant();
   if constexpr (G < 32 && NV == 1) {
-    if (kv != 1) {  // narrow rows: lock-step warp kernel
-      if (czero) spmm_lockstep<T, VEC, G, true><<<blocks, kThreads, 0, s>>>(a);
-      else spmm_lockstep<T, VEC, G, false><<<blocks, kThreads, 0, s>>>(a);
-      spmm_fixup<T, VEC, G, NV><<<fix_blocks, kThreads, 0, s>>>(a);
+    if (kv != 1) {
+      if (czero) spmm_vec<T, VEC, G, true, SEG><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_vec<T, VEC, G, false, SEG><<<blocks, kThreads, 0, s>>>(a);
       return;
     }
   }
@@ -590,21 +603,30 @@ void launch(const SpmmArgs<T>& a, bool czero, int blocks, int fix_blocks,
   const bool occ4 = G == 32 && NV == 1 && (ov == 4 || (ov == 0 && !use_rows));
   if (use_rows) {
     if (occ4) {
-      if (czero) spmm_rows<T, VEC, G, NV, true, 4><<<blocks, kThreads, 0, s>>>(a);
-      else spmm_rows<T, VEC, G, NV, false, 4><<<blocks, kThreads, 0, s>>>(a);
+      if (czero) spmm_rows<T, VEC, G, NV, true, 4, SEG><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_rows<T, VEC, G, NV, false, 4, SEG><<<blocks, kThreads, 0, s>>>(a);
     } else {
-      if (czero) spmm_rows<T, VEC, G, NV, true, 1><<<blocks, kThreads, 0, s>>>(a);
-      else spmm_rows<T, VEC, G, NV, false, 1><<<blocks, kThreads, 0, s>>>(a);
+      if (czero) spmm_rows<T, VEC, G, NV, true, 1, SEG><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_rows<T, VEC, G, NV, false, 1, SEG><<<blocks, kThreads, 0, s>>>(a);
     }
   } else {
     if (occ4) {
-      if (czero) spmm_stream<T, VEC, G, NV, true, 4><<<blocks, kThreads, 0, s>>>(a);
-      else spmm_stream<T, VEC, G, NV, false, 4><<<blocks, kThreads, 0, s>>>(a);
+      if (czero) spmm_stream<T, VEC, G, NV, true, 4, SEG><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_stream<T, VEC, G, NV, false, 4, SEG><<<blocks, kThreads, 0, s>>>(a);
     } else {
-      if (czero) spmm_stream<T, VEC, G, NV, true, 1><<<blocks, kThreads, 0, s>>>(a);
-      else spmm_stream<T, VEC, G, NV, false, 1><<<blocks, kThreads, 0, s>>>(a);
+      if (czero) spmm_stream<T, VEC, G, NV, true, 1, SEG><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_stream<T, VEC, G, NV, false, 1, SEG><<<blocks, kThreads, 0, s>>>(a);
     }
   }
+}
+
+template <typename T, int VEC, int G, int NV>
+void launch(const SpmmArgs<T>& a, bool czero, int blocks, int fix_blocks,
+            cudaStream_t s) {
+  if (a.nseg)
+    launch_seg<T, VEC, G, NV, true>(a, czero, blocks, s);
+  else
+    launch_seg<T, VEC, G, NV, false>(a, czero, blocks, s);
   spmm_fixup<T, VEC, G, NV><<<fix_blocks, kThreads, 0, s>>>(a);
 }
 
