@@ -59,7 +59,22 @@ def test_golden_real_valued(rd, golden, dt, tag, rel):
     got, _ = run(rd, h, b, c0)
     want = golden["spmm_real_c_" + tag]
     tol_check(got, want, h, b, c0, rel)
-    # rows not cut by a chunk boundary follow the reference's fma order exactly
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_wide_rows_follow_reference_fma_order(rd, orc, dt):
+    """For wide B rows (one 16-B vector per lane and more) the kernels keep the
+    reference's k-ascending fma chain from C for every row not cut by a chunk
+    boundary, so those rows are bitwise equal to the reference for real data."""
+    h = orc.rmat(10, 8, seed=1, dtype=dt)
+    h.values = oracle.real_twin(h.nnz, 3, dt)
+    n = 128 if dt == np.float32 else 64
+    b = oracle.real_twin(h.cols * n, 4, dt).reshape(h.cols, n)
+    c0 = oracle.real_twin(h.rows * n, 5, dt).reshape(h.rows, n)
+    want = c0.copy()
+    orc.spmm_local(h, b, want)
+    got, _ = run(rd, h, b, c0)
+    tol_check(got, want, h, b, c0, 1e-5 if dt == np.float32 else 1e-12)
     assert np.mean(np.all(got == want, axis=1)) > 0.5
 
 
