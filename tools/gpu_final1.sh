@@ -9,7 +9,6 @@ timeout 600 python bench.py --variant summa_nccl --no-cpu-baseline > $O/bench_cf
 timeout 900 python bench.py --impl reference > $O/ref_cfg3.json 2> $O/ref_cfg3.err
 timeout 900 python bench.py --impl reference --config cfg4 --steps 2 > $O/ref_cfg4.json 2> $O/ref_cfg4.err
 timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/plain.log 2>&1 && \
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_cfg3.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_launch.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm_stream -s 3 -c 1 -o $O/prof_spmm_cfg3 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_full.log 2>&1
-ls -la $O
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_cfg3.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_launch.log 2>&1
+ls -la $O; du -sh $O
 echo finished
