@@ -130,6 +130,10 @@ int rdmm_spmm_csr_seg(int dtype_bytes, uint32_t rows, uint32_t n, uint64_t nnz,
  * reference; values are summed in hardware order (exact for integer-valued
  * data, within rounding otherwise).  All operand pointers are device
  * pointers and must stay valid until rdmm_spgemm_numeric returns.
+ * A plan's working buffers live in the per-(device, stream) scratch pool, so
+ * they are reused across calls without cudaMalloc: run symbolic and numeric
+ * of one plan on the same stream, and do not interleave a second plan's
+ * symbolic on that stream between them.
  */
 typedef struct {
   const uint32_t* a_row_ptr; /* NULL: identity term */

@@ -666,20 +666,19 @@ int launch_dense_num(uint32_t slots, const uint32_t* list, uint32_t count,
   return RDMM_OK;
 }
 
+// Plan workspace: grow-only stream-ordered scratch per (device, stream,
+// slot) (common.cuh), so repeated products on one stream allocate nothing.
+// A stream has at most one SpGEMM plan in flight (symbolic -> numeric).
 struct Buf {
   void* p = nullptr;
   size_t n = 0;
-  ~Buf() {
-    if (p) cudaFree(p);
-  }
-  cudaError_t ensure(size_t bytes) {
-    if (n >= bytes && p) return cudaSuccess;
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-    cudaError_t e = cudaMalloc(&p, bytes ? bytes : 8);
-    if (e == cudaSuccess) n = bytes;
-    return e;
+  int slot = 0;
+  cudaError_t ensure(size_t bytes, cudaStream_t s) {
+    void* q = scratch(bytes ? bytes : 8, slot, s);
+    if (!q) return cudaErrorMemoryAllocation;
+    p = q;
+    n = bytes;
+    return cudaSuccess;
   }
   template <typename X>
   X* as() const {
@@ -744,6 +743,11 @@ struct rdmm_spgemm_plan {
   int nterms = 0;
   bool ident_only = false;
   Buf terms, cnt64, pre64, lists, tcount, ub, scan_tmp, bitmaps, dense;
+  rdmm_spgemm_plan() {
+    int slot = 10;
+    for (Buf* b : {&terms, &cnt64, &pre64, &lists, &tcount, &ub, &scan_tmp, &bitmaps, &dense})
+      b->slot = slot++;
+  }
   uint32_t sym_count[kTiers] = {0}, num_count[kTiers] = {0};
   uint64_t nnz = 0, flops = 0;
   std::vector<uint64_t> term_flops;
@@ -777,15 +781,15 @@ int symbolic_impl(uint32_t rows, uint32_t ncols, const rdmm_spgemm_term* terms,
       return fail(RDMM_ERR_INVALID, "spgemm: term without a B operand");
   }
   P->ident_only = ident_only;
-  RDMM_CUDA_TRY(P->terms.ensure(sizeof(TermDev<T>) * th.size()));
+  RDMM_CUDA_TRY(P->terms.ensure(sizeof(TermDev<T>) * th.size(), s));
   RDMM_CUDA_TRY(cudaMemcpyAsync(P->terms.p, th.data(),
                                 sizeof(TermDev<T>) * th.size(),
                                 cudaMemcpyHostToDevice, s));
-  RDMM_CUDA_TRY(P->cnt64.ensure(sizeof(uint64_t) * (size_t(rows) + 1)));
-  RDMM_CUDA_TRY(P->pre64.ensure(sizeof(uint64_t) * (size_t(rows) + 1)));
-  RDMM_CUDA_TRY(P->lists.ensure(sizeof(uint32_t) * size_t(kTiers) * (rows ? rows : 1)));
+  RDMM_CUDA_TRY(P->cnt64.ensure(sizeof(uint64_t) * (size_t(rows) + 1), s));
+  RDMM_CUDA_TRY(P->pre64.ensure(sizeof(uint64_t) * (size_t(rows) + 1), s));
+  RDMM_CUDA_TRY(P->lists.ensure(sizeof(uint32_t) * size_t(kTiers) * (rows ? rows : 1), s));
   const size_t tc_bytes = sizeof(uint32_t) * 2 * kTiers + 8 * size_t(nterms) + 16;
-  RDMM_CUDA_TRY(P->tcount.ensure(tc_bytes));
+  RDMM_CUDA_TRY(P->tcount.ensure(tc_bytes, s));
   RDMM_CUDA_TRY(cudaMemsetAsync(P->tcount.p, 0, tc_bytes, s));
   RDMM_CUDA_TRY(cudaMemsetAsync(P->cnt64.p, 0, sizeof(uint64_t) * (size_t(rows) + 1), s));
   uint32_t* tc = P->tcount.as<uint32_t>();
@@ -832,7 +836,7 @@ int symbolic_impl(uint32_t rows, uint32_t ncols, const rdmm_spgemm_term* terms,
       count_launch();
       fn<<<blocks, kDenseThreads, nwords * 4, s>>>(L(5), hc[5], td, nterms, cnt, nwords);
     } else {
-      RDMM_CUDA_TRY(P->bitmaps.ensure(size_t(blocks) * nwords * 4));
+      RDMM_CUDA_TRY(P->bitmaps.ensure(size_t(blocks) * nwords * 4, s));
       RDMM_CUDA_TRY(cudaMemsetAsync(P->bitmaps.p, 0, size_t(blocks) * nwords * 4, s));
       count_launch();
       k_dense_sym_global<T><<<blocks, kDenseThreads, 0, s>>>(
@@ -844,7 +848,7 @@ int symbolic_impl(uint32_t rows, uint32_t ncols, const rdmm_spgemm_term* terms,
   size_t tb = 0;
   RDMM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, P->pre64.as<uint64_t>(),
                                               int64_t(rows) + 1, s));
-  RDMM_CUDA_TRY(P->scan_tmp.ensure(tb));
+  RDMM_CUDA_TRY(P->scan_tmp.ensure(tb, s));
   RDMM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(P->scan_tmp.p, tb, cnt,
                                               P->pre64.as<uint64_t>(),
                                               int64_t(rows) + 1, s));
@@ -908,9 +912,9 @@ int numeric_impl(rdmm_spgemm_plan* P, uint32_t* cci, T* cv, cudaStream_t s) {
     const uint32_t nwords = uint32_t(ceil_div(P->ncols, 32));
     const int cl = dense_cl();
     const uint32_t blocks = dense_rows_in_flight(c[5], cl);
-    RDMM_CUDA_TRY(P->bitmaps.ensure(size_t(blocks) * nwords * 4));
+    RDMM_CUDA_TRY(P->bitmaps.ensure(size_t(blocks) * nwords * 4, s));
     RDMM_CUDA_TRY(cudaMemsetAsync(P->bitmaps.p, 0, size_t(blocks) * nwords * 4, s));
-    RDMM_CUDA_TRY(P->dense.ensure(size_t(blocks) * P->ncols * sizeof(T)));
+    RDMM_CUDA_TRY(P->dense.ensure(size_t(blocks) * P->ncols * sizeof(T), s));
     const size_t nd = size_t(blocks) * P->ncols;
     count_launch();
     k_fill<T><<<unsigned(std::min<uint64_t>(ceil_div(nd, 256), 4096)), 256, 0, s>>>(
