@@ -249,7 +249,8 @@ def run_ours(args, cfg, dev, rank, world):
         reset = Cm.init
     variant = args.variant
     opts = dict(variant=variant, ws_base="stationary_c", checksum=False, record_events=False,
-                fuse_k=not args.no_fuse, lookahead=args.lookahead)
+                fuse_k=not args.no_fuse, lookahead=args.lookahead,
+                split_local=not args.no_split)
     stream = torch.cuda.ExternalStream(f.stream(rank), device=dev)
 
     def barrier():
@@ -383,7 +384,7 @@ def run_ours(args, cfg, dev, rank, world):
         "data": "synthetic (reference generators, seeds A=1 B=2, built on device)",
         "config": {"workload": args.config, "desc": cfg["desc"], "rows": m, "cols": k, "n": n,
                    "nnz": nnz_a, "flop_per_step": total_flops,
-                   "variant": variant, "fuse_k": not args.no_fuse, "lookahead": args.lookahead, "grid": f"{pr}x{pc}", "tiles": [tm, tk, tn],
+                   "variant": variant, "fuse_k": not args.no_fuse, "split_local": not args.no_split, "lookahead": args.lookahead, "grid": f"{pr}x{pc}", "tiles": [tm, tk, tn],
                    "path": "run_multiply (host C-ABI rdmm_h_run_multiply) over the fabric",
                    "l2": ("inputs > L2 (A %.2f GB, B and C %.2f GB each)"
                           % (nnz_a * 8 / 1e9, m * n * 4 / 1e9)) if cfg["kind"] == "spmm"
@@ -612,6 +613,7 @@ def main():
     ap.add_argument("--ntiles", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fuse", action="store_true", help="RunOptions::fuse_k = false")
+    ap.add_argument("--no-split", action="store_true", help="RunOptions::split_local = false")
     ap.add_argument("--lookahead", type=int, default=2, help="RunOptions::lookahead")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

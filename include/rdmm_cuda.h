@@ -91,7 +91,8 @@ int rdmm_spmm_csr_f64(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
  *   RDMM_SPMM_C_ZERO      C is all-zero on entry (a fresh tile): rows with
  *                         nonzeros are written, C is never read; results are
  *                         identical to the accumulate form on a zero C.
- *   RDMM_SPMM_NO_PREFETCH disable the L2 prefetch of the next window's B rows.
+ *   RDMM_SPMM_NO_PREFETCH accepted for compatibility; no effect (the L2
+ *                         prefetch it disabled measured slower and was removed).
  */
 #define RDMM_SPMM_C_ZERO 1u
 #define RDMM_SPMM_NO_PREFETCH 2u

@@ -83,6 +83,7 @@ typedef struct {
   int ws_local_inplace;
   int checksum;
   int fuse_k;
+  int split_local; /* fused stationary-C: local products first on the first tile */
 } rdmm_h_options;
 
 #define RDMM_H_MAX_RANKS 64

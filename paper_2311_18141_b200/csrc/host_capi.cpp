@@ -95,6 +95,7 @@ RunOptions opts_of(const rdmm_h_options* o) {
   r.ws_local_inplace = o->ws_local_inplace != 0;
   r.checksum = o->checksum != 0;
   r.fuse_k = o->fuse_k != 0;
+  r.split_local = o->split_local != 0;
   return r;
 }
 

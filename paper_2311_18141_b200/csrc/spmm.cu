@@ -93,7 +93,7 @@ struct SpmmArgs {
   uint64_t ldb, ldc;
   uint64_t nnz, Q;
   uint32_t rows, nvec, nchunks, wstride;
-  int prefetch;
+  int prefetch;  // unused (the L2 prefetch of the next window measured slower)
   // Segmented B (fused K-tile products): B row g lives in segment
   // g / seg_rows at row g % seg_rows; nseg == 0 means one contiguous B.
   const T* bseg[16];
@@ -101,13 +101,29 @@ struct SpmmArgs {
   uint32_t nseg, seg_rows, seg_shift;
 };
 
+// Segment base pointers staged in shared memory once per CTA (indexing the
+// kernel-parameter array with a runtime segment number forces a local copy).
+template <typename T>
+struct SegTable {
+  const T* base[16];
+};
+
+template <typename T, bool SEG>
+__device__ __forceinline__ void load_segs(const SpmmArgs<T>& p, SegTable<T>& st) {
+  if constexpr (SEG) {
+    if (threadIdx.x < 16) st.base[threadIdx.x] = p.bseg[threadIdx.x] + p.boff;
+    __syncthreads();
+  }
+}
+
 template <typename T, typename V, bool SEG>
-__device__ __forceinline__ const V* brow_ptr(const SpmmArgs<T>& p, const V* Bv, uint32_t k,
-                                             uint64_t ldbv, uint32_t voff) {
+__device__ __forceinline__ const V* brow_ptr(const SpmmArgs<T>& p, const SegTable<T>& st,
+                                             const V* Bv, uint32_t k, uint64_t ldbv,
+                                             uint32_t voff) {
   if constexpr (!SEG) return Bv + uint64_t(k) * ldbv + voff;
   const uint32_t sg = p.seg_shift < 32 ? (k >> p.seg_shift) : (k / p.seg_rows);
   const uint32_t r = k - sg * p.seg_rows;
-  return reinterpret_cast<const V*>(p.bseg[sg] + p.boff) + uint64_t(r) * ldbv + voff;
+  return reinterpret_cast<const V*>(st.base[sg]) + uint64_t(r) * ldbv + voff;
 }
 
 template <int G>
@@ -161,8 +177,8 @@ __device__ __forceinline__ void win_load(uint32_t (&rew)[SL],
 }
 
 // Stream one nnz chunk [lo, hi): the chunk's nonzeros are consumed 32 at a
-// time regardless of row boundaries (col/val of the next window and an L2
-// prefetch of its B rows overlap the current window's gathers), rows are
+// time regardless of row boundaries (col/val of the next window load while
+// the current window's gathers are in flight), rows are
 // tracked through a 32-entry window of row ends held in registers, and a row
 // is flushed to C (or to a carry slot if the chunk cuts it) when the stream
 // crosses its end.  CZERO: C is known to be zero on entry (first product
@@ -171,6 +187,8 @@ template <typename T, int VEC, int G, int NV, bool CZERO, int MINB, bool SEG>
 __global__ void __launch_bounds__(kThreads, MINB)
     spmm_stream(const SpmmArgs<T> p) {
   using V = typename VecOf<T, VEC>::type;
+  __shared__ SegTable<T> segs;
+  load_segs<T, SEG>(p, segs);
   constexpr int SL = kWin / G;  // staged entries per lane
   const unsigned gm = group_mask<G>();
   const uint32_t lane = threadIdx.x % G;
@@ -179,7 +197,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
   const V* __restrict__ Bv = reinterpret_cast<const V*>(p.B);
   V* __restrict__ Cv = reinterpret_cast<V*>(p.C);
   const uint64_t ldbv = p.ldb / VEC, ldcv = p.ldc / VEC;
-  const uint32_t row_bytes = p.nvec * VEC * sizeof(T);
   bool colok[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) colok[v] = lane + G * v < p.nvec;
@@ -238,22 +255,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
             const int q = t + u;
             const uint32_t k = __shfl_sync(gm, kk[q / G], q % G, G);
             if (q < int(cnt)) {
-              const V* brow = brow_ptr<T, V, SEG>(p, Bv, k, ldbv, lane);
+              const V* brow = brow_ptr<T, V, SEG>(p, segs, Bv, k, ldbv, lane);
 #pragma unroll
               for (int v = 0; v < NV; ++v)
                 if (colok[v]) bv[u][v] = __ldg(brow + G * v);
-            }
-          }
-          if (t == kU && p.prefetch) {
-            // warm L2 with the next window's B rows (no registers held)
-#pragma unroll
-            for (int j = 0; j < SL; ++j) {
-              if (w + kWin + lane + G * j < hi) {
-                const char* rowp = reinterpret_cast<const char*>(
-                    Bv + uint64_t(kn[j]) * ldbv);
-                for (uint32_t off = 0; off < row_bytes; off += 128)
-                  asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + off));
-              }
             }
           }
 #pragma unroll
@@ -333,6 +338,8 @@ template <typename T, int VEC, int G, int NV, bool CZERO, int MINB, bool SEG>
 __global__ void __launch_bounds__(kThreads, MINB)
     spmm_rows(const SpmmArgs<T> p) {
   using V = typename VecOf<T, VEC>::type;
+  __shared__ SegTable<T> segs;
+  load_segs<T, SEG>(p, segs);
   constexpr int SL = kWin / G;
   const unsigned gm = group_mask<G>();
   const uint32_t lane = threadIdx.x % G;
@@ -390,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
                 const int q = t + u;
                 const uint32_t k = __shfl_sync(gm, kk[q / G], q % G, G);
                 if (q < int(cnt)) {
-                  const V* brow = brow_ptr<T, V, SEG>(p, Bv, k, ldbv, lane);
+                  const V* brow = brow_ptr<T, V, SEG>(p, segs, Bv, k, ldbv, lane);
 #pragma unroll
                   for (int v = 0; v < NV; ++v)
                     if (colok[v]) bv[u][v] = __ldg(brow + G * v);
@@ -442,6 +449,8 @@ template <typename T, int VEC, int L, bool CZERO, bool SEG>
 __global__ void __launch_bounds__(kThreads)
     spmm_vec(const SpmmArgs<T> p) {
   using V = typename VecOf<T, VEC>::type;
+  __shared__ SegTable<T> segs;
+  load_segs<T, SEG>(p, segs);
   constexpr int S = 32 / L;
   constexpr int U = 4;
   const uint32_t lane = threadIdx.x & 31u, sl = lane / L, v = lane % L;
@@ -486,7 +495,7 @@ __global__ void __launch_bounds__(kThreads)
                 const int q = t + u * S + int(sl);
                 const uint32_t k = __shfl_sync(0xffffffffu, kk, q & 31);
                 av[u] = __shfl_sync(0xffffffffu, aa, q & 31);
-                if (q < int(cnt) && colok) bv[u] = __ldg(brow_ptr<T, V, SEG>(p, Bv, k, ldbv, v));
+                if (q < int(cnt) && colok) bv[u] = __ldg(brow_ptr<T, V, SEG>(p, segs, Bv, k, ldbv, v));
               }
 #pragma unroll
               for (int u = 0; u < U; ++u) {
@@ -557,23 +566,8 @@ __global__ void __launch_bounds__(kThreads) spmm_fixup(const SpmmArgs<T> p) {
   }
 }
 
-struct Plan {
-  int G = 32, NV = 1, blocks = 0;
-  uint32_t nchunks = 0;
-  uint64_t Q = 0;
-};
-
-// RDMM_SPMM_OCC=1|4 forces the unconstrained / 64-register (4 CTAs/SM)
-// build of the main kernel (dev switch; default auto).
-inline int occ_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("RDMM_SPMM_OCC");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
-
-// RDMM_SPMM_KERNEL=rows|stream forces a kernel (dev switch; default auto).
+// RDMM_SPMM_KERNEL=rows|stream forces a kernel (dev switch; default auto;
+// narrow rows accept only "rows").
 inline int kernel_variant() {
   static const int v = [] {
     const char* e = std::getenv("RDMM_SPMM_KERNEL");
@@ -590,32 +584,27 @@ void launch_seg(const SpmmArgs<T>& a, bool czero, int blocks, cudaStream_t s) {
   // wider rows (NV>=2) keep more gathers in flight per lane and the
   // row-oriented kernel is faster there (at the HBM gather roofline on ER);
   // narrow rows (N<128) use the whole-warp row kernel.
+  // Only the (kernel, occupancy) pairs that a setting can select are
+  // instantiated: narrow rows -> spmm_vec (or spmm_rows when forced);
+  // G=32,NV=1 -> 4 CTAs/SM; wider -> 1 CTA/SM minimum.
   const int kv = kernel_variant();
-  if constexpr (G < 32 && NV == 1) {
-    if (kv != 1) {
-      if (czero) spmm_vec<T, VEC, G, true, SEG><<<blocks, kThreads, 0, s>>>(a);
-      else spmm_vec<T, VEC, G, false, SEG><<<blocks, kThreads, 0, s>>>(a);
-      return;
-    }
-  }
-  const bool use_rows = kv == 1 || (kv == 0 && !(G == 32 && NV == 1));
-  const int ov = occ_variant();
-  const bool occ4 = G == 32 && NV == 1 && (ov == 4 || (ov == 0 && !use_rows));
-  if (use_rows) {
-    if (occ4) {
-      if (czero) spmm_rows<T, VEC, G, NV, true, 4, SEG><<<blocks, kThreads, 0, s>>>(a);
-      else spmm_rows<T, VEC, G, NV, false, 4, SEG><<<blocks, kThreads, 0, s>>>(a);
-    } else {
+  if constexpr (G < 32) {
+    if (kv == 1) {
       if (czero) spmm_rows<T, VEC, G, NV, true, 1, SEG><<<blocks, kThreads, 0, s>>>(a);
       else spmm_rows<T, VEC, G, NV, false, 1, SEG><<<blocks, kThreads, 0, s>>>(a);
+    } else {
+      if (czero) spmm_vec<T, VEC, G, true, SEG><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_vec<T, VEC, G, false, SEG><<<blocks, kThreads, 0, s>>>(a);
     }
   } else {
-    if (occ4) {
-      if (czero) spmm_stream<T, VEC, G, NV, true, 4, SEG><<<blocks, kThreads, 0, s>>>(a);
-      else spmm_stream<T, VEC, G, NV, false, 4, SEG><<<blocks, kThreads, 0, s>>>(a);
+    constexpr int MB = NV == 1 ? 4 : 1;
+    const bool use_rows = kv == 1 || (kv == 0 && NV != 1);
+    if (use_rows) {
+      if (czero) spmm_rows<T, VEC, G, NV, true, MB, SEG><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_rows<T, VEC, G, NV, false, MB, SEG><<<blocks, kThreads, 0, s>>>(a);
     } else {
-      if (czero) spmm_stream<T, VEC, G, NV, true, 1, SEG><<<blocks, kThreads, 0, s>>>(a);
-      else spmm_stream<T, VEC, G, NV, false, 1, SEG><<<blocks, kThreads, 0, s>>>(a);
+      if (czero) spmm_stream<T, VEC, G, NV, true, MB, SEG><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_stream<T, VEC, G, NV, false, MB, SEG><<<blocks, kThreads, 0, s>>>(a);
     }
   }
 }
@@ -712,14 +701,6 @@ size_t workspace_bytes_impl(uint32_t rows, uint64_t nnz, uint32_t n) {
                   make_plan<T>(nnz, n, false).bytes);
 }
 
-inline int prefetch_default() {
-  static const int v = [] {
-    const char* e = std::getenv("RDMM_SPMM_PREFETCH");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
-
 template <typename T>
 int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
               const uint32_t* rp, const uint32_t* ci, const T* val, const T* B,
@@ -761,7 +742,6 @@ int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
   a.rows = rows;
   a.nchunks = P.nchunks;
   a.wstride = P.wstride;
-  a.prefetch = (flags & RDMM_SPMM_NO_PREFETCH) ? 0 : prefetch_default();
   a.nseg = nseg;
   a.seg_rows = seg_rows;
   a.seg_shift = 32;

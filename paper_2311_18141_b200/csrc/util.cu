@@ -82,32 +82,78 @@ struct ConcatArgs {
   uint64_t col_stride;
 };
 
+// The tile pointer tables are staged in shared memory: indexing the
+// kernel-parameter arrays with a runtime k would copy them to local memory.
+__device__ __forceinline__ void stage_args(const ConcatArgs& a, ConcatArgs& sa) {
+  if (threadIdx.x < 16) {
+    sa.rp[threadIdx.x] = a.rp[threadIdx.x];
+    sa.ci[threadIdx.x] = a.ci[threadIdx.x];
+    sa.val[threadIdx.x] = a.val[threadIdx.x];
+  }
+  if (threadIdx.x == 0) {
+    sa.K = a.K;
+    sa.col_stride = a.col_stride;
+  }
+  __syncthreads();
+}
+
 __global__ void k_concat_rowptr(ConcatArgs a, uint32_t rows, uint32_t* out_rp) {
+  __shared__ ConcatArgs sa;
+  stage_args(a, sa);
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r <= rows;
        r += gridDim.x * blockDim.x) {
     uint32_t s = 0;
-    for (uint32_t k = 0; k < a.K; ++k) s += a.rp[k][r];
+    for (uint32_t k = 0; k < sa.K; ++k) s += __ldg(sa.rp[k] + r);
     out_rp[r] = s;
   }
 }
 
+// A warp owns 32 consecutive rows.  For each tile k those rows' nonzeros are
+// one contiguous input range, streamed 32 at a time with coalesced loads;
+// each lane finds the row of its element by a binary search over the 32 row
+// starts held in the warp's registers and writes it after the row's earlier
+// tiles in the output row.
 template <typename T>
 __global__ void k_concat_fill(ConcatArgs a, uint32_t rows, const uint32_t* out_rp,
                               uint32_t* out_ci, T* out_val) {
+  __shared__ ConcatArgs sa;
+  stage_args(a, sa);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t r = w; r < rows; r += nw) {
-    uint32_t o = out_rp[r];
-    for (uint32_t k = 0; k < a.K; ++k) {
-      const uint32_t s = a.rp[k][r], e = a.rp[k][r + 1];
-      const uint32_t off = uint32_t(k * a.col_stride);
-      const T* v = static_cast<const T*>(a.val[k]);
-      for (uint32_t q = lane; q < e - s; q += 32) {
-        out_ci[o + q] = a.ci[k][s + q] + off;
-        out_val[o + q] = v[s + q];
+  for (uint64_t r0 = uint64_t(w) * 32; r0 < rows; r0 += uint64_t(nw) * 32) {
+    const uint32_t r = uint32_t(r0) + lane;
+    const bool ok = r < rows;
+    uint32_t base = ok ? __ldg(out_rp + r) : 0u;
+    for (uint32_t k = 0; k < sa.K; ++k) {
+      const uint32_t* rp = sa.rp[k];
+      const uint32_t* ci = sa.ci[k];
+      const T* v = static_cast<const T*>(sa.val[k]);
+      const uint32_t off = uint32_t(k * sa.col_stride);
+      const uint32_t end_all = __ldg(rp + rows);
+      const uint32_t s = ok ? __ldg(rp + r) : end_all;
+      const uint32_t e = ok ? __ldg(rp + r + 1) : end_all;
+      const uint32_t lo = __shfl_sync(0xffffffffu, s, 0);
+      const uint32_t last = min(31u, rows - 1 - uint32_t(r0));
+      const uint32_t hi_v = __shfl_sync(0xffffffffu, e, last);
+      for (uint32_t q0 = lo; q0 < hi_v; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        // largest row j with start_j <= q
+        uint32_t j = 0;
+#pragma unroll
+        for (uint32_t step = 16; step >= 1; step >>= 1) {
+          const uint32_t sj = __shfl_sync(0xffffffffu, s, j + step);
+          if (q >= sj) j += step;
+        }
+        const uint32_t bj = __shfl_sync(0xffffffffu, base, j);
+        const uint32_t sj = __shfl_sync(0xffffffffu, s, j);
+        if (q < hi_v) {
+          const uint32_t d = bj + (q - sj);
+          out_ci[d] = __ldg(ci + q) + off;
+          out_val[d] = __ldg(v + q);
+        }
       }
-      o += e - s;
+      base += e - s;
     }
   }
 }
@@ -225,7 +271,7 @@ extern "C" int rdmm_csr_concat_cols(int dtype_bytes, uint32_t rows, uint32_t K,
   count_launch(2);
   k_concat_rowptr<<<b1, 256, 0, s>>>(a, rows, out_rp);
   const unsigned b2 = unsigned(std::max<uint64_t>(
-      1, std::min<uint64_t>(ceil_div(rows, 8), uint64_t(num_sms()) * 16)));
+      1, std::min<uint64_t>(ceil_div(rows, 256), uint64_t(num_sms()) * 8)));
   if (dtype_bytes == 8)
     k_concat_fill<double><<<b2, 256, 0, s>>>(a, rows, out_rp, out_ci, static_cast<double*>(out_val));
   else

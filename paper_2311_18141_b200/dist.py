@@ -25,7 +25,8 @@ class Options(C.Structure):
                 ("offset", C.c_int), ("seed", C.c_uint64), ("delay_ns_per_flop", C.c_double),
                 ("random_delay_ms_max", C.c_double), ("record_events", C.c_int),
                 ("record_triples", C.c_int), ("lookahead", C.c_int),
-                ("ws_local_inplace", C.c_int), ("checksum", C.c_int), ("fuse_k", C.c_int)]
+                ("ws_local_inplace", C.c_int), ("checksum", C.c_int), ("fuse_k", C.c_int),
+                ("split_local", C.c_int)]
 
 
 class Report(C.Structure):
@@ -279,12 +280,13 @@ class RunReport:
 def run_multiply(f: Fabric, A: DistSparse, B, Cm, variant="stationary_c", ws_base="stationary_a",
                  prefetch=True, offset=True, seed=0, delay_ns_per_flop=0.0,
                  random_delay_ms_max=0.0, record_events=True, record_triples=False,
-                 lookahead=2, ws_local_inplace=True, checksum=True, fuse_k=True) -> RunReport:
+                 lookahead=2, ws_local_inplace=True, checksum=True, fuse_k=True,
+                 split_local=True) -> RunReport:
     """C += A*B on the fabric -- algos.hpp:673-752."""
     o = Options(VARIANTS.index(variant), VARIANTS.index(ws_base), int(prefetch), int(offset),
                 seed, delay_ns_per_flop, random_delay_ms_max, int(record_events),
                 int(record_triples), lookahead, int(ws_local_inplace), int(checksum),
-                int(fuse_k))
+                int(fuse_k), int(split_local))
     r = Report()
     L.check(_h.rdmm_h_run_multiply(f._h, A._h, B._h, Cm._h, C.byref(o), C.byref(r)),
             "run_multiply")

@@ -186,6 +186,28 @@ def extract_tile(g: DeviceCsr, r0: int, nrows: int, c0: int, ncols: int,
     return out
 
 
+def concat_cols(tiles, col_stride: int, stream=None) -> DeviceCsr:
+    """[A_0 | A_1 | ...]: same-height CSR tiles side by side, tile k's columns
+    shifted by k * col_stride (the fused stationary-C operand, algos.hpp:378-415)."""
+    if not tiles or len(tiles) > 16:
+        raise ValueError("concat_cols: 1..16 tiles")
+    t0 = tiles[0]
+    if any(t.rows != t0.rows or t.dtype != t0.dtype for t in tiles):
+        raise L.DimensionError("concat_cols: tiles differ in rows or dtype")
+    nnz = sum(t.nnz for t in tiles)
+    cols = col_stride * (len(tiles) - 1) + tiles[-1].cols
+    out = DeviceCsr.empty(t0.rows, cols, nnz, dtype=t0.dtype, device=t0.device)
+    K = len(tiles)
+    rp = (C.c_void_p * K)(*[t.row_ptr.data_ptr() for t in tiles])
+    ci = (C.c_void_p * K)(*[t.col_idx.data_ptr() if t.nnz else 0 for t in tiles])
+    vv = (C.c_void_p * K)(*[t.values.data_ptr() if t.nnz else 0 for t in tiles])
+    L.check(L.rdmm_csr_concat_cols(_wcode(t0.dtype), t0.rows, K, rp, ci, vv, col_stride,
+                                   out.row_ptr.data_ptr(), out.col_idx.data_ptr() if nnz else None,
+                                   out.values.data_ptr() if nnz else None, _stream(stream)),
+            "concat_cols")
+    return out
+
+
 def dense_add_into(c: torch.Tensor, x: torch.Tensor, stream=None) -> None:
     """c += x (tile.hpp:300-307)."""
     if c.shape != x.shape:

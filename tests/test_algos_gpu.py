@@ -117,6 +117,8 @@ def test_offset_and_prefetch_toggles(dist, orc):
     no_off, _, _ = run_spmm(dist, orc, variant="stationary_c", offset=False)
     no_pre, _, _ = run_spmm(dist, orc, variant="stationary_c", prefetch=False)
     no_fuse, _, _ = run_spmm(dist, orc, variant="stationary_c", fuse_k=False)
+    no_split, _, _ = run_spmm(dist, orc, variant="stationary_c", split_local=False)
+    assert np.array_equal(no_split, base)
     assert np.array_equal(base, want) and np.array_equal(no_off, base)
     assert np.array_equal(no_pre, base) and np.array_equal(no_fuse, base)
     a_off, want2, _ = run_spmm(dist, orc, variant="stationary_a", offset=False)

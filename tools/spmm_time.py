@@ -1,5 +1,5 @@
 """Time spmm_local on a BASELINE config (dev tool; env vars select kernel
-variants: RDMM_SPMM_PREFETCH, RDMM_SPMM_OCC)."""
+variants: RDMM_SPMM_PREFETCH, RDMM_SPMM_KERNEL)."""
 import argparse
 import json
 import os
