@@ -97,63 +97,79 @@ __device__ __forceinline__ void stage_args(const ConcatArgs& a, ConcatArgs& sa) 
   __syncthreads();
 }
 
-__global__ void k_concat_rowptr(ConcatArgs a, uint32_t rows, uint32_t* out_rp) {
+// Row pass: out_rp[r] = sum_k rp_k[r], and for every tile k the shift
+// D_k[r] that moves tile k's nonzero q of row r to its output slot
+// D_k[r] + q, i.e. D_k[r] = sum_{k'<k} rp_k'[r+1] + sum_{k'>k} rp_k'[r].
+__global__ void k_concat_rows(ConcatArgs a, uint32_t rows, uint32_t* __restrict__ out_rp,
+                              uint32_t* __restrict__ shift) {
   __shared__ ConcatArgs sa;
   stage_args(a, sa);
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r <= rows;
        r += gridDim.x * blockDim.x) {
-    uint32_t s = 0;
-    for (uint32_t k = 0; k < sa.K; ++k) s += __ldg(sa.rp[k] + r);
-    out_rp[r] = s;
+    uint32_t total = 0;
+    for (uint32_t k = 0; k < sa.K; ++k) total += __ldg(sa.rp[k] + r);
+    out_rp[r] = total;
+    if (r == rows) continue;
+    uint32_t before = 0;  // sum_{k'<k} rp_k'[r+1]
+    uint32_t after = total;  // sum_{k'>=k} rp_k'[r]
+    for (uint32_t k = 0; k < sa.K; ++k) {
+      const uint32_t s0 = __ldg(sa.rp[k] + r);
+      after -= s0;
+      shift[uint64_t(k) * rows + r] = before + after;
+      before += __ldg(sa.rp[k] + r + 1);
+    }
   }
 }
 
-// A warp owns 32 consecutive rows.  For each tile k those rows' nonzeros are
-// one contiguous input range, streamed 32 at a time with coalesced loads;
-// each lane finds the row of its element by a binary search over the 32 row
-// starts held in the warp's registers and writes it after the row's earlier
-// tiles in the output row.
+// Element pass for tile k: every warp copies chunks of kChunk consecutive
+// nonzeros (coalesced loads, balanced however long the rows are); the row of
+// each element comes from a 32-row window of row starts held in registers
+// (binary search by shuffles), advanced as the chunk crosses row ends.
+constexpr uint32_t kConcatChunk = 2048;
+
 template <typename T>
-__global__ void k_concat_fill(ConcatArgs a, uint32_t rows, const uint32_t* out_rp,
-                              uint32_t* out_ci, T* out_val) {
-  __shared__ ConcatArgs sa;
-  stage_args(a, sa);
+__global__ void k_concat_fill(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                              const T* __restrict__ val, uint32_t rows, uint32_t off,
+                              const uint32_t* __restrict__ shift, uint32_t* __restrict__ out_ci,
+                              T* __restrict__ out_val) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint64_t r0 = uint64_t(w) * 32; r0 < rows; r0 += uint64_t(nw) * 32) {
-    const uint32_t r = uint32_t(r0) + lane;
-    const bool ok = r < rows;
-    uint32_t base = ok ? __ldg(out_rp + r) : 0u;
-    for (uint32_t k = 0; k < sa.K; ++k) {
-      const uint32_t* rp = sa.rp[k];
-      const uint32_t* ci = sa.ci[k];
-      const T* v = static_cast<const T*>(sa.val[k]);
-      const uint32_t off = uint32_t(k * sa.col_stride);
-      const uint32_t end_all = __ldg(rp + rows);
-      const uint32_t s = ok ? __ldg(rp + r) : end_all;
-      const uint32_t e = ok ? __ldg(rp + r + 1) : end_all;
-      const uint32_t lo = __shfl_sync(0xffffffffu, s, 0);
-      const uint32_t last = min(31u, rows - 1 - uint32_t(r0));
-      const uint32_t hi_v = __shfl_sync(0xffffffffu, e, last);
-      for (uint32_t q0 = lo; q0 < hi_v; q0 += 32) {
-        const uint32_t q = q0 + lane;
-        // largest row j with start_j <= q
+  const uint32_t nnz = __ldg(rp + rows);
+  for (uint64_t c0 = uint64_t(w) * kConcatChunk; c0 < nnz; c0 += uint64_t(nw) * kConcatChunk) {
+    const uint32_t q0 = uint32_t(c0);
+    const uint32_t q1 = uint32_t(min(c0 + kConcatChunk, uint64_t(nnz)));
+    // row holding q0: largest r with rp[r] <= q0
+    uint32_t lo = 0, hi = rows;
+    while (hi - lo > 1) {
+      const uint32_t m = (lo + hi) >> 1;
+      if (__ldg(rp + m) <= q0) lo = m; else hi = m;
+    }
+    uint32_t r = lo, qb = q0;
+    while (qb < q1) {
+      const uint32_t rr = r + lane;
+      const bool ok = rr < rows;
+      const uint32_t s = ok ? __ldg(rp + rr) : 0xFFFFFFFFu;
+      const uint32_t e = ok ? __ldg(rp + rr + 1) : 0xFFFFFFFFu;
+      const uint32_t d = ok ? __ldg(shift + rr) : 0u;
+      const uint32_t wend = __shfl_sync(0xffffffffu, e, 31);
+      const uint32_t lim = min(q1, wend);
+      for (; qb < lim; qb += 32) {
+        const uint32_t q = qb + lane;
         uint32_t j = 0;
 #pragma unroll
         for (uint32_t step = 16; step >= 1; step >>= 1) {
           const uint32_t sj = __shfl_sync(0xffffffffu, s, j + step);
           if (q >= sj) j += step;
         }
-        const uint32_t bj = __shfl_sync(0xffffffffu, base, j);
-        const uint32_t sj = __shfl_sync(0xffffffffu, s, j);
-        if (q < hi_v) {
-          const uint32_t d = bj + (q - sj);
-          out_ci[d] = __ldg(ci + q) + off;
-          out_val[d] = __ldg(v + q);
+        const uint32_t dj = __shfl_sync(0xffffffffu, d, j);
+        if (q < lim) {
+          out_ci[dj + q] = __ldg(ci + q) + off;
+          out_val[dj + q] = __ldg(val + q);
         }
       }
-      base += e - s;
+      qb = lim;
+      r += 32;
     }
   }
 }
@@ -257,6 +273,8 @@ extern "C" int rdmm_csr_concat_cols(int dtype_bytes, uint32_t rows, uint32_t K,
                                     uint32_t* out_rp, uint32_t* out_ci,
                                     void* out_val, rdmm_stream_t stream) {
   if (K == 0 || K > 16) return fail(RDMM_ERR_INVALID, "concat: 1..16 tiles");
+  if (col_stride * (K - 1) > 0xFFFFFFFFull)
+    return fail(RDMM_ERR_INVALID, "concat: concatenated columns exceed index_t");
   ConcatArgs a{};
   for (uint32_t k = 0; k < K; ++k) {
     a.rp[k] = rp[k];
@@ -266,16 +284,27 @@ extern "C" int rdmm_csr_concat_cols(int dtype_bytes, uint32_t rows, uint32_t K,
   a.K = K;
   a.col_stride = col_stride;
   cudaStream_t s = as_stream(stream);
+  auto* shift = static_cast<uint32_t*>(scratch(size_t(K) * std::max<uint32_t>(rows, 1) * 4, 4, s));
+  if (!shift) return fail(RDMM_ERR_CUDA, "concat: scratch allocation failed");
   const unsigned b1 = unsigned(std::max<uint64_t>(
       1, std::min<uint64_t>(ceil_div(uint64_t(rows) + 1, 256), uint64_t(num_sms()) * 8)));
-  count_launch(2);
-  k_concat_rowptr<<<b1, 256, 0, s>>>(a, rows, out_rp);
-  const unsigned b2 = unsigned(std::max<uint64_t>(
-      1, std::min<uint64_t>(ceil_div(rows, 256), uint64_t(num_sms()) * 8)));
-  if (dtype_bytes == 8)
-    k_concat_fill<double><<<b2, 256, 0, s>>>(a, rows, out_rp, out_ci, static_cast<double*>(out_val));
-  else
-    k_concat_fill<float><<<b2, 256, 0, s>>>(a, rows, out_rp, out_ci, static_cast<float*>(out_val));
+  count_launch(1 + K);
+  k_concat_rows<<<b1, 256, 0, s>>>(a, rows, out_rp, shift);
+  if (rows) {
+    const unsigned b2 = unsigned(num_sms()) * 8;
+    for (uint32_t k = 0; k < K; ++k) {
+      const uint32_t off = uint32_t(k * col_stride);
+      const uint32_t* sh = shift + uint64_t(k) * rows;
+      if (dtype_bytes == 8)
+        k_concat_fill<double><<<b2, 256, 0, s>>>(rp[k], ci[k], static_cast<const double*>(val[k]),
+                                                 rows, off, sh, out_ci,
+                                                 static_cast<double*>(out_val));
+      else
+        k_concat_fill<float><<<b2, 256, 0, s>>>(rp[k], ci[k], static_cast<const float*>(val[k]),
+                                                rows, off, sh, out_ci,
+                                                static_cast<float*>(out_val));
+    }
+  }
   RDMM_CUDA_TRY(cudaGetLastError());
   return RDMM_OK;
 }
