@@ -99,53 +99,8 @@ struct SpmmArgs {
   const T* bseg[16];
   uint64_t boff;  // element offset applied to every segment (column panel)
   uint32_t nseg, seg_rows, seg_shift;
-  // L2 residency hints (HINT kernels): bit k of `hot` marks a frequently
-  // gathered B row; hot rows load with pol_mode's first policy, the rest
-  // with its second (1: evict_last/evict_first, 2: normal/evict_first,
-  // 3: evict_last/normal).
-  const uint32_t* __restrict__ hot;
-  int hint_mode;
 };
 
-template <typename V>
-__device__ __forceinline__ V ldg_pol(const V* p, uint64_t pol);
-template <>
-__device__ __forceinline__ float4 ldg_pol(const float4* p, uint64_t pol) {
-  float4 r;
-  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-      : "l"(p), "l"(pol));
-  return r;
-}
-template <>
-__device__ __forceinline__ double2 ldg_pol(const double2* p, uint64_t pol) {
-  double2 r;
-  asm("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-      : "=d"(r.x), "=d"(r.y)
-      : "l"(p), "l"(pol));
-  return r;
-}
-template <>
-__device__ __forceinline__ float ldg_pol(const float* p, uint64_t pol) {
-  float r;
-  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
-  return r;
-}
-template <>
-__device__ __forceinline__ double ldg_pol(const double* p, uint64_t pol) {
-  double r;
-  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
-  return r;
-}
-
-__device__ __forceinline__ void make_policies(int mode, uint64_t& hot, uint64_t& cold) {
-  uint64_t last, normal, first;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(last));
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(normal));
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(first));
-  hot = mode == 2 ? normal : last;
-  cold = mode == 3 ? normal : first;
-}
 
 // Segment base pointers staged in shared memory once per CTA (indexing the
 // kernel-parameter array with a runtime segment number forces a local copy).
@@ -229,7 +184,7 @@ __device__ __forceinline__ void win_load(uint32_t (&rew)[SL],
 // is flushed to C (or to a carry slot if the chunk cuts it) when the stream
 // crosses its end.  CZERO: C is known to be zero on entry (first product
 // into a fresh tile), so C is written but never read.
-template <typename T, int VEC, int G, int NV, bool CZERO, int MINB, bool SEG, bool HINT>
+template <typename T, int VEC, int G, int NV, bool CZERO, int MINB, bool SEG>
 __global__ void __launch_bounds__(kThreads, MINB)
     spmm_stream(const SpmmArgs<T> p) {
   using V = typename VecOf<T, VEC>::type;
@@ -246,8 +201,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
   bool colok[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) colok[v] = lane + G * v < p.nvec;
-  uint64_t pol_hot = 0, pol_cold = 0;
-  if constexpr (HINT) make_policies(p.hint_mode, pol_hot, pol_cold);
 
   for (uint32_t c = worker; c < p.nchunks; c += nworkers) {
     const uint64_t lo = uint64_t(c) * p.Q;
@@ -282,12 +235,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
       kk[j] = ok ? __ldcs(p.ci + idx) : 0u;
       aa[j] = ok ? __ldcs(p.val + idx) : T(0);
     }
-    // hot-row bitmap words of the staged columns (HINT), one window ahead
-    uint32_t hw[SL], hn[SL];
-    if constexpr (HINT) {
-#pragma unroll
-      for (int j = 0; j < SL; ++j) hw[j] = __ldg(p.hot + (kk[j] >> 5));
-    }
     for (uint64_t w = lo; w < hi; w += kWin) {
       const uint32_t cnt = uint32_t(umin(kWin, hi - w));
       // next window's col/val (software pipelined one window ahead)
@@ -308,29 +255,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
           for (int u = 0; u < kU; ++u) {
             const int q = t + u;
             const uint32_t k = __shfl_sync(gm, kk[q / G], q % G, G);
-            if constexpr (HINT) {
-              const uint32_t word = __shfl_sync(gm, hw[q / G], q % G, G);
-              const uint64_t pol = ((word >> (k & 31)) & 1u) ? pol_hot : pol_cold;
-              if (q < int(cnt)) {
-                const V* brow = brow_ptr<T, V, SEG>(p, segs, Bv, k, ldbv, lane);
+            if (q < int(cnt)) {
+              const V* brow = brow_ptr<T, V, SEG>(p, segs, Bv, k, ldbv, lane);
 #pragma unroll
-                for (int v = 0; v < NV; ++v)
-                  if (colok[v]) bv[u][v] = ldg_pol(brow + G * v, pol);
-              }
-            } else {
-              if (q < int(cnt)) {
-                const V* brow = brow_ptr<T, V, SEG>(p, segs, Bv, k, ldbv, lane);
-#pragma unroll
-                for (int v = 0; v < NV; ++v)
-                  if (colok[v]) bv[u][v] = __ldg(brow + G * v);
-              }
-            }
-          }
-          if constexpr (HINT) {
-            if (t == kU) {
-              // the next window's columns have landed by now
-#pragma unroll
-              for (int j = 0; j < SL; ++j) hn[j] = __ldg(p.hot + (kn[j] >> 5));
+              for (int v = 0; v < NV; ++v)
+                if (colok[v]) bv[u][v] = __ldg(brow + G * v);
             }
           }
 #pragma unroll
@@ -384,10 +313,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
       for (int j = 0; j < SL; ++j) {
         kk[j] = kn[j];
         aa[j] = an[j];
-        if constexpr (HINT) {
-          // windows shorter than kU + 1 never reached the t == kU load
-          hw[j] = cnt > uint32_t(kU) ? hn[j] : __ldg(p.hot + (kn[j] >> 5));
-        }
       }
     }
     // the chunk's last row
@@ -653,109 +578,6 @@ inline int kernel_variant() {
   return v;
 }
 
-// ---- hot-row bitmap for the L2 residency hints.  Column frequencies are
-// estimated from every 2^sl-th nonzero; the most frequent columns whose B
-// rows fit in the L2 budget get their bit set.
-__global__ void k_hot_sample(const uint32_t* __restrict__ ci, uint64_t nnz, uint32_t sl,
-                             uint32_t cols, uint32_t* __restrict__ cnt) {
-  const uint64_t n = (nnz + (1ull << sl) - 1) >> sl;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t k = __ldg(ci + (i << sl));
-    if (k < cols) atomicAdd(cnt + k, 1u);
-  }
-}
-
-__global__ void k_hot_hist(const uint32_t* __restrict__ cnt, uint32_t cols,
-                           uint32_t* __restrict__ bins) {
-  __shared__ uint32_t sb[256];
-  for (int b = threadIdx.x; b < 256; b += blockDim.x) sb[b] = 0;
-  __syncthreads();
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cols;
-       c += gridDim.x * blockDim.x) {
-    const uint32_t v = min(__ldg(cnt + c), 255u);
-    if (v) atomicAdd(sb + v, 1u);
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < 256; b += blockDim.x)
-    if (sb[b]) atomicAdd(bins + b, sb[b]);
-}
-
-__global__ void k_hot_pick(uint32_t* bins, uint32_t budget_rows) {
-  uint32_t acc = 0, t = 256;
-  for (int b = 255; b >= 1; --b) {
-    if (acc + bins[b] > budget_rows) break;
-    acc += bins[b];
-    t = uint32_t(b);
-  }
-  bins[0] = t;
-}
-
-__global__ void k_hot_bits(const uint32_t* __restrict__ cnt, uint32_t cols,
-                           const uint32_t* __restrict__ bins, uint32_t* __restrict__ bm) {
-  const uint32_t t = bins[0];
-  const uint32_t words = (cols + 31) / 32;
-  for (uint32_t base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; base < words * 32u;
-       base += gridDim.x * blockDim.x) {
-    const uint32_t c = base + (threadIdx.x & 31u);
-    const bool hot = c < cols && __ldg(cnt + c) >= t;
-    const unsigned m = __ballot_sync(0xffffffffu, hot);
-    if ((threadIdx.x & 31u) == 0) bm[base / 32] = m;
-  }
-}
-
-// RDMM_SPMM_L2HINT=0|1|2|3 (hint_mode; default 0 = off) and
-// RDMM_SPMM_L2HOT_MB (budget of hot B rows, default 64).
-inline int hint_mode_env() {
-  static const int v = [] {
-    const char* e = std::getenv("RDMM_SPMM_L2HINT");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
-inline uint64_t hint_budget_bytes() {
-  static const uint64_t v = [] {
-    const char* e = std::getenv("RDMM_SPMM_L2HOT_MB");
-    return (e ? uint64_t(std::atoll(e)) : 64ull) << 20;
-  }();
-  return v;
-}
-
-// Builds the bitmap on stream s (slots 20-21); returns nullptr on failure.
-inline const uint32_t* build_hot(const uint32_t* ci, uint64_t nnz, uint32_t cols,
-                                 uint64_t row_bytes, cudaStream_t s) {
-  const uint32_t words = (cols + 31) / 32;
-  auto* cnt = static_cast<uint32_t*>(scratch(size_t(cols) * 4, 20, s));
-  auto* bins = static_cast<uint32_t*>(scratch(256 * 4 + size_t(words) * 4, 21, s));
-  if (!cnt || !bins) return nullptr;
-  uint32_t* bm = bins + 256;
-  if (cudaMemsetAsync(cnt, 0, size_t(cols) * 4, s) != cudaSuccess ||
-      cudaMemsetAsync(bins, 0, 256 * 4, s) != cudaSuccess)
-    return nullptr;
-  const int sms = num_sms();
-  const uint32_t budget = uint32_t(std::min<uint64_t>(hint_budget_bytes() / row_bytes, cols));
-  count_launch(4);
-  k_hot_sample<<<sms * 4, 256, 0, s>>>(ci, nnz, 4, cols, cnt);
-  k_hot_hist<<<sms * 2, 256, 0, s>>>(cnt, cols, bins);
-  k_hot_pick<<<1, 1, 0, s>>>(bins, budget);
-  k_hot_bits<<<sms * 2, 256, 0, s>>>(cnt, cols, bins, bm);
-  return cudaGetLastError() == cudaSuccess ? bm : nullptr;
-}
-
-template <typename T, int VEC, int G, int NV, int MB, bool SEG>
-void launch_stream(const SpmmArgs<T>& a, bool czero, int blocks, cudaStream_t s) {
-  if constexpr (NV == 1) {
-    if (a.hot) {
-      // the hint state needs the 80-register (3 CTAs/SM) build
-      if (czero) spmm_stream<T, VEC, G, NV, true, 3, SEG, true><<<blocks, kThreads, 0, s>>>(a);
-      else spmm_stream<T, VEC, G, NV, false, 3, SEG, true><<<blocks, kThreads, 0, s>>>(a);
-      return;
-    }
-  }
-  if (czero) spmm_stream<T, VEC, G, NV, true, MB, SEG, false><<<blocks, kThreads, 0, s>>>(a);
-  else spmm_stream<T, VEC, G, NV, false, MB, SEG, false><<<blocks, kThreads, 0, s>>>(a);
-}
-
 template <typename T, int VEC, int G, int NV, bool SEG>
 void launch_seg(const SpmmArgs<T>& a, bool czero, int blocks, cudaStream_t s) {
   // Measured on B200 (profiles/): the nnz-stream kernel at
@@ -782,7 +604,8 @@ void launch_seg(const SpmmArgs<T>& a, bool czero, int blocks, cudaStream_t s) {
       if (czero) spmm_rows<T, VEC, G, NV, true, MB, SEG><<<blocks, kThreads, 0, s>>>(a);
       else spmm_rows<T, VEC, G, NV, false, MB, SEG><<<blocks, kThreads, 0, s>>>(a);
     } else {
-      launch_stream<T, VEC, G, NV, MB, SEG>(a, czero, blocks, s);
+      if (czero) spmm_stream<T, VEC, G, NV, true, MB, SEG><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_stream<T, VEC, G, NV, false, MB, SEG><<<blocks, kThreads, 0, s>>>(a);
     }
   }
 }
@@ -926,16 +749,6 @@ int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
     if (seg_rows == 0) return fail(RDMM_ERR_INVALID, "spmm: seg_rows must be positive");
     for (uint32_t q = 0; q < nseg; ++q) a.bseg[q] = bseg[q];
     if ((seg_rows & (seg_rows - 1)) == 0) a.seg_shift = uint32_t(__builtin_ctz(seg_rows));
-  }
-  a.hot = nullptr;
-  a.hint_mode = hint_mode_env();
-  {
-    // hints pay only when B does not fit in L2 and the G=32, NV=1 stream
-    // kernel runs (one 16-B vector per lane)
-    const uint64_t row_bytes = uint64_t(P.pv) * P.VEC * sizeof(T);
-    const bool stream_kernel = P.pv == 32 && kernel_variant() != 1;
-    if (a.hint_mode && stream_kernel && uint64_t(cols) * row_bytes > (96ull << 20))
-      a.hot = build_hot(ci, nnz, cols, row_bytes, s);
   }
   char* base = static_cast<char*>(w);
   const size_t vbytes = size_t(P.nchunks) * P.wstride * sizeof(T);
