@@ -296,12 +296,14 @@ FlopMeter spmm_fused(rdmm_fabric* f, std::uint32_t rank, const std::vector<DevCs
   if (K == 1) return spmm_local<T>(a[0], b[0], c, stream, c_zero);
   std::uint64_t nnz = 0;
   std::vector<const index_t*> rp(K), ci(K);
+  std::vector<std::uint64_t> tn(K);
   std::vector<const void*> vv(K), bs(K);
   for (std::size_t k = 0; k < K; ++k) {
     if (a[k].rows != c.rows || a[k].cols != b[k].rows || b[k].cols != c.cols ||
         b[k].ld != b[0].ld || (k + 1 < K && b[k].rows != col_stride))
       throw dimension_error("spmm_fused: dimension mismatch");
     nnz += a[k].nnz;
+    tn[k] = a[k].nnz;
     rp[k] = a[k].row_ptr;
     ci[k] = a[k].col_idx;
     vv[k] = a[k].values;
@@ -311,7 +313,7 @@ FlopMeter spmm_fused(rdmm_fabric* f, std::uint32_t rank, const std::vector<DevCs
   DevBuffer cci(f, rank, nnz * sizeof(index_t), stream);
   DevBuffer cvv(f, rank, nnz * sizeof(T), stream);
   check(rdmm_csr_concat_cols(dtype_bytes<T>(), c.rows, std::uint32_t(K), rp.data(), ci.data(),
-                             vv.data(), col_stride, static_cast<index_t*>(crp.get()),
+                             vv.data(), tn.data(), col_stride, static_cast<index_t*>(crp.get()),
                              static_cast<index_t*>(cci.get()), cvv.get(), stream),
         "spmm_fused concat");
   std::uint64_t fl = 0;

@@ -82,8 +82,8 @@ rdmm_csr_extract_count = _fn("rdmm_csr_extract_count", [vp, vp, u64, u32, u64, u
                                                         vp])
 rdmm_csr_extract_fill = _fn("rdmm_csr_extract_fill", [cint, vp, vp, vp, u64, u32, u64, u32, vp,
                                                       vp, vp, vp])
-rdmm_csr_concat_cols = _fn("rdmm_csr_concat_cols", [cint, u32, u32, vp, vp, vp, u64, vp, vp, vp,
-                                                    vp])
+rdmm_csr_concat_cols = _fn("rdmm_csr_concat_cols", [cint, u32, u32, vp, vp, vp, vp, u64, vp, vp,
+                                                    vp, vp])
 rdmm_spmm_workspace_bytes = _fn("rdmm_spmm_workspace_bytes", [u32, u64, u32, cint], sz)
 _spmm_args = [u32, u32, u32, u64, vp, vp, vp, vp, u64, vp, u64, vp, sz, vp, P(u64)]
 rdmm_spmm_csr_f32 = _fn("rdmm_spmm_csr_f32", _spmm_args)

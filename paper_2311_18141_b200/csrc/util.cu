@@ -100,8 +100,11 @@ __device__ __forceinline__ void stage_args(const ConcatArgs& a, ConcatArgs& sa) 
 // Row pass: out_rp[r] = sum_k rp_k[r], and for every tile k the shift
 // D_k[r] that moves tile k's nonzero q of row r to its output slot
 // D_k[r] + q, i.e. D_k[r] = sum_{k'<k} rp_k'[r+1] + sum_{k'>k} rp_k'[r].
+constexpr uint32_t kConcatChunk = 2048;
+
 __global__ void k_concat_rows(ConcatArgs a, uint32_t rows, uint32_t* __restrict__ out_rp,
-                              uint32_t* __restrict__ shift) {
+                              uint32_t* __restrict__ shift, uint32_t* __restrict__ chunk_row,
+                              uint32_t chunk_stride) {
   __shared__ ConcatArgs sa;
   stage_args(a, sa);
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r <= rows;
@@ -114,58 +117,71 @@ __global__ void k_concat_rows(ConcatArgs a, uint32_t rows, uint32_t* __restrict_
     uint32_t after = total;  // sum_{k'>=k} rp_k'[r]
     for (uint32_t k = 0; k < sa.K; ++k) {
       const uint32_t s0 = __ldg(sa.rp[k] + r);
+      const uint32_t e0 = __ldg(sa.rp[k] + r + 1);
       after -= s0;
       shift[uint64_t(k) * rows + r] = before + after;
-      before += __ldg(sa.rp[k] + r + 1);
+      before += e0;
+      // this row holds the first nonzero of chunks ceil(s0/C) .. (e0-1)/C
+      for (uint32_t c = (s0 + kConcatChunk - 1) / kConcatChunk; e0 > s0 && c <= (e0 - 1) / kConcatChunk;
+           ++c)
+        chunk_row[uint64_t(k) * chunk_stride + c] = r;
     }
   }
 }
 
-// Element pass for tile k: every warp copies chunks of kChunk consecutive
-// nonzeros (coalesced loads, balanced however long the rows are); the row of
+// Element pass for tile k: every warp copies chunks of kConcatChunk
+// consecutive nonzeros (coalesced loads, balanced however long the rows are;
+// the row pass recorded the row of each chunk's first nonzero); the row of
 // each element comes from a 32-row window of row starts held in registers
 // (binary search by shuffles), advanced as the chunk crosses row ends.
-constexpr uint32_t kConcatChunk = 2048;
-
 template <typename T>
 __global__ void k_concat_fill(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
                               const T* __restrict__ val, uint32_t rows, uint32_t off,
-                              const uint32_t* __restrict__ shift, uint32_t* __restrict__ out_ci,
+                              const uint32_t* __restrict__ shift,
+                              const uint32_t* __restrict__ chunk_row, uint32_t* __restrict__ out_ci,
                               T* __restrict__ out_val) {
+  constexpr int U = 4;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t nnz = __ldg(rp + rows);
-  for (uint64_t c0 = uint64_t(w) * kConcatChunk; c0 < nnz; c0 += uint64_t(nw) * kConcatChunk) {
-    const uint32_t q0 = uint32_t(c0);
-    const uint32_t q1 = uint32_t(min(c0 + kConcatChunk, uint64_t(nnz)));
-    // row holding q0: largest r with rp[r] <= q0
-    uint32_t lo = 0, hi = rows;
-    while (hi - lo > 1) {
-      const uint32_t m = (lo + hi) >> 1;
-      if (__ldg(rp + m) <= q0) lo = m; else hi = m;
-    }
-    uint32_t r = lo, qb = q0;
+  const uint32_t nch = (nnz + kConcatChunk - 1) / kConcatChunk;
+  for (uint32_t c = w; c < nch; c += nw) {
+    const uint32_t q0 = c * kConcatChunk;
+    const uint32_t q1 = min(q0 + kConcatChunk, nnz);
+    uint32_t r = __ldg(chunk_row + c), qb = q0;
     while (qb < q1) {
       const uint32_t rr = r + lane;
       const bool ok = rr < rows;
       const uint32_t s = ok ? __ldg(rp + rr) : 0xFFFFFFFFu;
       const uint32_t e = ok ? __ldg(rp + rr + 1) : 0xFFFFFFFFu;
       const uint32_t d = ok ? __ldg(shift + rr) : 0u;
-      const uint32_t wend = __shfl_sync(0xffffffffu, e, 31);
-      const uint32_t lim = min(q1, wend);
-      for (; qb < lim; qb += 32) {
-        const uint32_t q = qb + lane;
-        uint32_t j = 0;
+      const uint32_t lim = min(q1, __shfl_sync(0xffffffffu, e, 31));
+      for (; qb < lim; qb += 32 * U) {
+        uint32_t cv[U];
+        T vv[U];
 #pragma unroll
-        for (uint32_t step = 16; step >= 1; step >>= 1) {
-          const uint32_t sj = __shfl_sync(0xffffffffu, s, j + step);
-          if (q >= sj) j += step;
+        for (int u = 0; u < U; ++u) {
+          const uint32_t q = qb + 32 * u + lane;
+          if (q < lim) {
+            cv[u] = __ldg(ci + q);
+            vv[u] = __ldg(val + q);
+          }
         }
-        const uint32_t dj = __shfl_sync(0xffffffffu, d, j);
-        if (q < lim) {
-          out_ci[dj + q] = __ldg(ci + q) + off;
-          out_val[dj + q] = __ldg(val + q);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t q = qb + 32 * u + lane;
+          uint32_t j = 0;
+#pragma unroll
+          for (uint32_t step = 16; step >= 1; step >>= 1) {
+            const uint32_t sj = __shfl_sync(0xffffffffu, s, j + step);
+            if (q >= sj) j += step;
+          }
+          const uint32_t dj = __shfl_sync(0xffffffffu, d, j);
+          if (q < lim) {
+            out_ci[dj + q] = cv[u] + off;
+            out_val[dj + q] = vv[u];
+          }
         }
       }
       qb = lim;
@@ -269,7 +285,8 @@ extern "C" int rdmm_spin_delay(uint64_t ns, rdmm_stream_t stream) {
 extern "C" int rdmm_csr_concat_cols(int dtype_bytes, uint32_t rows, uint32_t K,
                                     const uint32_t* const* rp,
                                     const uint32_t* const* ci,
-                                    const void* const* val, uint64_t col_stride,
+                                    const void* const* val, const uint64_t* tile_nnz,
+                                    uint64_t col_stride,
                                     uint32_t* out_rp, uint32_t* out_ci,
                                     void* out_val, rdmm_stream_t stream) {
   if (K == 0 || K > 16) return fail(RDMM_ERR_INVALID, "concat: 1..16 tiles");
@@ -284,24 +301,42 @@ extern "C" int rdmm_csr_concat_cols(int dtype_bytes, uint32_t rows, uint32_t K,
   a.K = K;
   a.col_stride = col_stride;
   cudaStream_t s = as_stream(stream);
-  auto* shift = static_cast<uint32_t*>(scratch(size_t(K) * std::max<uint32_t>(rows, 1) * 4, 4, s));
+  // chunk table: one entry per kConcatChunk nonzeros of the largest tile
+  uint64_t max_nnz_bound = 0;
+  for (uint32_t k = 0; k < K; ++k) {
+    uint64_t n = 0;
+    if (tile_nnz) {
+      n = tile_nnz[k];
+    } else {
+      uint32_t n32 = 0;
+      RDMM_CUDA_TRY(cudaMemcpyAsync(&n32, rp[k] + rows, 4, cudaMemcpyDeviceToHost, s));
+      RDMM_CUDA_TRY(cudaStreamSynchronize(s));
+      n = n32;
+    }
+    max_nnz_bound = std::max<uint64_t>(max_nnz_bound, n);
+  }
+  const uint32_t cstride = uint32_t(ceil_div(std::max<uint64_t>(max_nnz_bound, 1), kConcatChunk));
+  const size_t shift_bytes = size_t(K) * std::max<uint32_t>(rows, 1) * 4;
+  auto* shift = static_cast<uint32_t*>(scratch(shift_bytes + size_t(K) * cstride * 4, 4, s));
   if (!shift) return fail(RDMM_ERR_CUDA, "concat: scratch allocation failed");
+  uint32_t* chunk_row = shift + size_t(K) * std::max<uint32_t>(rows, 1);
   const unsigned b1 = unsigned(std::max<uint64_t>(
       1, std::min<uint64_t>(ceil_div(uint64_t(rows) + 1, 256), uint64_t(num_sms()) * 8)));
   count_launch(1 + K);
-  k_concat_rows<<<b1, 256, 0, s>>>(a, rows, out_rp, shift);
+  k_concat_rows<<<b1, 256, 0, s>>>(a, rows, out_rp, shift, chunk_row, cstride);
   if (rows) {
     const unsigned b2 = unsigned(num_sms()) * 8;
     for (uint32_t k = 0; k < K; ++k) {
       const uint32_t off = uint32_t(k * col_stride);
       const uint32_t* sh = shift + uint64_t(k) * rows;
+      const uint32_t* cr = chunk_row + uint64_t(k) * cstride;
       if (dtype_bytes == 8)
         k_concat_fill<double><<<b2, 256, 0, s>>>(rp[k], ci[k], static_cast<const double*>(val[k]),
-                                                 rows, off, sh, out_ci,
+                                                 rows, off, sh, cr, out_ci,
                                                  static_cast<double*>(out_val));
       else
         k_concat_fill<float><<<b2, 256, 0, s>>>(rp[k], ci[k], static_cast<const float*>(val[k]),
-                                                rows, off, sh, out_ci,
+                                                rows, off, sh, cr, out_ci,
                                                 static_cast<float*>(out_val));
     }
   }

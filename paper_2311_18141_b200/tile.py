@@ -201,7 +201,8 @@ def concat_cols(tiles, col_stride: int, stream=None) -> DeviceCsr:
     rp = (C.c_void_p * K)(*[t.row_ptr.data_ptr() for t in tiles])
     ci = (C.c_void_p * K)(*[t.col_idx.data_ptr() if t.nnz else 0 for t in tiles])
     vv = (C.c_void_p * K)(*[t.values.data_ptr() if t.nnz else 0 for t in tiles])
-    L.check(L.rdmm_csr_concat_cols(_wcode(t0.dtype), t0.rows, K, rp, ci, vv, col_stride,
+    nz = (C.c_uint64 * K)(*[t.nnz for t in tiles])
+    L.check(L.rdmm_csr_concat_cols(_wcode(t0.dtype), t0.rows, K, rp, ci, vv, nz, col_stride,
                                    out.row_ptr.data_ptr(), out.col_idx.data_ptr() if nnz else None,
                                    out.values.data_ptr() if nnz else None, _stream(stream)),
             "concat_cols")
