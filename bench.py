@@ -132,26 +132,39 @@ def load_traffic(config, kernel, n_gpus):
 def layout(cfg, P, args):
     """ProcGrid and tile sizes for P ranks.
 
-    SpMM: a 1 x P grid (B and C split by columns, K = P column tiles of A)
-    keeps every rank's compute identical and moves only A tiles (SURVEY
-    §8(e)).  SpGEMM: a P x 1 grid with 4P row tiles of C and K = P, so the
+    SpMM: a P x 1 grid (A and C split by rows, K = P row tiles of B).  Each
+    rank keeps the full-width (N = 128) nnz-bound stream kernel and runs its
+    local product A(i,i) B(i,0) first while the copy engines fetch the other
+    B tiles over NVLink (stationary-C offset k = (i+j) % K, lookahead 2).
+    A 1 x P grid (column split) replicates A instead but drops every rank to
+    the narrow N/P kernel, whose cost follows the 4M rows it walks, not the
+    nonzeros: measured 2x slower at P = 2 (profiles/README.md).
+    SpGEMM: a P x 1 grid with 4P row tiles of C and K = P, so the
     locality-aware work stealing can rebalance R-MAT's row skew.
     """
     n_rows = 1 << cfg["scale"]
     if args.grid:
         pr, pc = (int(x) for x in args.grid.split("x"))
-    elif cfg["kind"] == "spmm":
-        pr, pc = 1, P
     else:
         pr, pc = P, 1
     mt = args.mtiles or (pr if cfg["kind"] == "spmm" else 4 * pr)
-    kt = args.ktiles or (pc if cfg["kind"] == "spmm" else pr)
+    kt = args.ktiles or (max(pr, pc) if cfg["kind"] == "spmm" else pr)
     ncols = cfg["n"] if cfg["kind"] == "spmm" else n_rows
     nt = args.ntiles or pc
     return (pr, pc), (-(-n_rows // mt), -(-n_rows // kt), -(-ncols // nt))
 
 
 # ----------------------------------------------------------------- our arm
+
+
+def owned_dense_bytes(grid, rows, cols, tr, tc, rank):
+    """fp32 bytes of the dense tiles `rank` owns (ProcGrid owner rule)."""
+    tot = 0
+    for i in range(-(-rows // tr)):
+        for j in range(-(-cols // tc)):
+            if grid.owner(i, j) == rank:
+                tot += (min(rows, (i + 1) * tr) - i * tr) * (min(cols, (j + 1) * tc) - j * tc) * 4
+    return tot
 
 
 def gen_inputs(cfg, dev):
@@ -221,6 +234,7 @@ def run_ours(args, cfg, dev, rank, world):
     tdist = torch.distributed if world > 1 else None
     a, b = gen_inputs(cfg, dev)
     m, k, nnz_a = a.rows, a.cols, a.nnz
+    rp_host = a.row_ptr.cpu().numpy().view("uint32")
     n = cfg["n"] if cfg["kind"] == "spmm" else a.cols
     (pr, pc), (tm, tk, tn) = layout(cfg, world, args)
     grid = dm.ProcGrid(pr, pc)
@@ -310,10 +324,19 @@ def run_ours(args, cfg, dev, rank, world):
     # ---- roofline of the dominant kernel on this rank
     hbm, peak_src = peaks()
     if cfg["kind"] == "spmm":
-        own_cols = min(tn, n)
         ktiles = -(-k // tk)
-        # per-rank compulsory bytes: all A tiles once, own B and C columns once
-        alg = 4 * (m + 1) * ktiles + 8 * nnz_a + 4 * k * own_cols + 4 * m * own_cols
+        # per-rank compulsory bytes over the owned C tiles (i, j): the A row
+        # block's tiles once (row_ptr per k tile + col/val), B(:, j) once, C
+        # tile written once
+        alg = 0
+        for i in range(-(-m // tm)):
+            for j in range(-(-n // tn)):
+                if grid.owner(i, j) != rank:
+                    continue
+                r0, r1 = i * tm, min(m, (i + 1) * tm)
+                cols = min(n, (j + 1) * tn) - j * tn
+                nnz_i = int(rp_host[r1]) - int(rp_host[r0])
+                alg += 4 * (r1 - r0 + 1) * ktiles + 8 * nnz_i + 4 * k * cols + 4 * (r1 - r0) * cols
         kernel = "spmm_stream+spmm_fixup (rdmm_spmm_csr), all launches of a step on this rank"
     else:
         alg = (2 * a_bytes + (m + 1) * 4 + 8 * (out_nnz or 0)) // world
@@ -351,13 +374,13 @@ def run_ours(args, cfg, dev, rank, world):
         h2d = sum(x.numel() * x.element_size() for x in (rp_h, ci_h, vv_h))
         if cfg["kind"] == "spmm":
             B.init_from_device(b_h)  # pinned host -> this rank's B tiles
-            h2d += k * min(tn, n) * 4
+            h2d += owned_dense_bytes(grid, k, n, tk, tn, rank)
         else:
             B.init_from_device(a_dev)
         dm.run_multiply(f, A, B, Cm, **opts)
         if cfg["kind"] == "spmm":
             Cm.owned_to_host(c_h)
-            d2h = m * min(tn, n) * 4
+            d2h = owned_dense_bytes(grid, m, n, tm, tn, rank)
         else:
             d2h = Cm.owned_to_host(c_h)
         torch.cuda.synchronize()

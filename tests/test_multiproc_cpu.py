@@ -100,7 +100,9 @@ def test_bench_session_and_layout():
         mtiles = ktiles = ntiles = 0
 
     (pr, pc), tiles = bench.layout(bench.CONFIGS["cfg3"], 8, A)
-    assert (pr, pc) == (1, 8) and tiles == [4194304, 524288, 16] or tiles == (4194304, 524288, 16)
+    assert (pr, pc) == (8, 1) and tuple(tiles) == (524288, 524288, 128)
+    (pr, pc), tiles = bench.layout(bench.CONFIGS["cfg3"], 1, A)
+    assert (pr, pc) == (1, 1) and tuple(tiles) == (4194304, 4194304, 128)
     (pr, pc), tiles = bench.layout(bench.CONFIGS["cfg4"], 4, A)
     assert (pr, pc) == (4, 1) and tiles[0] == (1 << 20) // 16
     assert bench.make_session(1, 0) is None
