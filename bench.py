@@ -132,8 +132,10 @@ def load_traffic(config, kernel, n_gpus):
 def layout(cfg, P, args):
     """ProcGrid and tile sizes for P ranks.
 
-    SpMM: a P x 1 grid (A and C split by rows, K = P row tiles of B).  Each
-    rank keeps the full-width (N = 128) nnz-bound stream kernel and runs its
+    SpMM: split B/C columns only while each rank keeps >= 128 fp32 columns
+    (cfg5, N = 256: 1 x 2, then 2 x 2 ...), the rest of P splits A/C rows
+    (cfg3, N = 128: P x 1, K = P row tiles of B).  Each rank keeps the
+    full-width nnz-bound stream kernel and runs its
     local product A(i,i) B(i,0) first while the copy engines fetch the other
     B tiles over NVLink (stationary-C offset k = (i+j) % K, lookahead 2).
     A 1 x P grid (column split) replicates A instead but drops every rank to
@@ -146,7 +148,11 @@ def layout(cfg, P, args):
     if args.grid:
         pr, pc = (int(x) for x in args.grid.split("x"))
     else:
-        pr, pc = P, 1
+        # split columns only while every rank keeps >= 128 fp32 columns
+        pc = 1
+        while cfg["kind"] == "spmm" and P % (2 * pc) == 0 and cfg["n"] // (2 * pc) >= 128:
+            pc *= 2
+        pr = P // pc
     mt = args.mtiles or (pr if cfg["kind"] == "spmm" else 4 * pr)
     kt = args.ktiles or (max(pr, pc) if cfg["kind"] == "spmm" else pr)
     ncols = cfg["n"] if cfg["kind"] == "spmm" else n_rows

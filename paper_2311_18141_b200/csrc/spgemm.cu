@@ -173,12 +173,9 @@ __device__ __forceinline__ void enumerate_row(uint32_t r,
 }
 
 // Heavy rows: each warp of the CTA (and of the `nparts` CTAs sharing the
-// row) takes 32 consecutive A entries at a time (coalesced col/val and
-// independent B row_ptr loads, one per lane), prefix-sums their B-row lengths
-// and streams the flattened products 64 per step: lane p finds its entry by a
-// 5-step shuffle search, so short B rows do not idle lanes and the loads of
-// two products per lane are in flight before they are inserted.  Used by the
-// large CTA tiers and the dense tier.
+// row) takes whole A entries, its lanes stride over the entry's B row
+// (coalesced, no search); two products per lane are loaded before they are
+// inserted.  Used by the large CTA tiers and the dense tier.
 template <typename T, int G, bool kValues, class Ins>
 __device__ __forceinline__ void enumerate_row_warps(uint32_t r, const TermDev<T>* terms,
                                                     int nterms, Ins ins, uint32_t part = 0,
@@ -188,55 +185,29 @@ __device__ __forceinline__ void enumerate_row_warps(uint32_t r, const TermDev<T>
   const uint32_t gw = part * W + wid, nw = nparts * W;
   for (int t = 0; t < nterms; ++t) {
     const TermDev<T> tm = terms[t];
-    if (tm.arp == nullptr) {  // identity term: B row r as-is
-      if (gw != 0) continue;
-      const uint32_t bs = __ldg(tm.brp + r), be = __ldg(tm.brp + r + 1);
-      for (uint32_t q = bs + lane; q < be; q += 32)
-        ins(__ldg(tm.bci + q), kValues ? __ldg(tm.bv + q) : T(0));
-      continue;
-    }
-    const uint32_t s0 = __ldg(tm.arp + r), s1 = __ldg(tm.arp + r + 1);
-    for (uint32_t e0 = s0 + gw * 32; e0 < s1; e0 += nw * 32) {
-      const uint32_t e = e0 + lane;
-      const bool ok = e < s1;
-      const uint32_t k = ok ? __ldg(tm.aci + e) : 0u;
-      T a = T(0);
-      if (kValues && ok) a = __ldg(tm.av + e);
-      const uint32_t bs = ok ? __ldg(tm.brp + k) : 0u;
-      const uint32_t len = ok ? __ldg(tm.brp + k + 1) - bs : 0u;
-      uint32_t incl = len;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t x = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= uint32_t(d)) incl += x;
-      }
-      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      const uint32_t excl = incl - len;
-      for (uint32_t p0 = 0; p0 < total; p0 += 64) {
-        uint32_t key[2];
-        T val[2];
-        bool valid[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t p = p0 + 32 * h + lane;
-          uint32_t j = 0;
-#pragma unroll
-          for (uint32_t step = 16; step >= 1; step >>= 1) {
-            const uint32_t xj = __shfl_sync(0xffffffffu, excl, j + step);
-            if (xj <= p) j += step;
+    const bool ident = tm.arp == nullptr;
+    const uint32_t s0 = ident ? 0u : __ldg(tm.arp + r);
+    const uint32_t s1 = ident ? 1u : __ldg(tm.arp + r + 1);
+    for (uint32_t e = s0 + gw; e < s1; e += nw) {
+      const uint32_t k = ident ? r : __ldg(tm.aci + e);
+      T a = T(1);
+      if (kValues && !ident) a = __ldg(tm.av + e);
+      const uint32_t bs = __ldg(tm.brp + k), be = __ldg(tm.brp + k + 1);
+      for (uint32_t q = bs + lane; q < be; q += 64) {
+        const bool two = q + 32 < be;
+        const uint32_t k0 = __ldg(tm.bci + q);
+        const uint32_t k1 = two ? __ldg(tm.bci + q + 32) : 0u;
+        T v0 = T(0), v1 = T(0);
+        if (kValues) {
+          v0 = __ldg(tm.bv + q);
+          if (two) v1 = __ldg(tm.bv + q + 32);
+          if (!ident) {
+            v0 = a * v0;
+            v1 = a * v1;
           }
-          const uint32_t bj = __shfl_sync(0xffffffffu, bs, j);
-          const uint32_t xj = __shfl_sync(0xffffffffu, excl, j);
-          const T aj = __shfl_sync(0xffffffffu, a, j);
-          valid[h] = p < total;
-          const uint32_t q = bj + (p - xj);
-          key[h] = valid[h] ? __ldg(tm.bci + q) : 0u;
-          val[h] = T(0);
-          if (kValues && valid[h]) val[h] = aj * __ldg(tm.bv + q);
         }
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          if (valid[h]) ins(key[h], val[h]);
+        ins(k0, v0);
+        if (two) ins(k1, v1);
       }
     }
   }
