@@ -289,7 +289,7 @@ __global__ void k_bin_num(uint32_t rows, const uint64_t* cnt64, uint32_t* lists,
 template <typename T, int TAB, int G>
 __global__ void __launch_bounds__(G == 32 ? 256 : G)
     k_sym_hash(const uint32_t* __restrict__ list, uint32_t count,
-               const TermDev<T>* terms, int nterms, uint64_t* cnt64) {
+               const TermDev<T>* terms, int nterms, uint64_t* cnt64, int flat) {
   constexpr int RPB = G == 32 ? 8 : 1;  // rows per block
   constexpr int LOG2T = __builtin_ctz(TAB);
   extern __shared__ __align__(16) unsigned char smem[];
@@ -309,13 +309,17 @@ __global__ void __launch_bounds__(G == 32 ? 256 : G)
     auto sym_ins = [&](uint32_t key, T) {
         uint32_t s = hslot(key, LOG2T);
         for (;;) {
-          const uint32_t old = atomicCAS(keys + s, kEmpty, key);
-          if (old == kEmpty || old == key) break;
+          const uint32_t cur = reinterpret_cast<volatile uint32_t*>(keys)[s];
+          if (cur == key) break;
+          if (cur == kEmpty) {
+            const uint32_t old = atomicCAS(keys + s, kEmpty, key);
+            if (old == kEmpty || old == key) break;
+          }
           s = (s + 1) & (TAB - 1);
         }
     };
     if (active) {
-      if constexpr (G >= 512)
+      if (G >= 512 && !flat)
         enumerate_row_warps<T, G, false>(r, terms, nterms, sym_ins);
       else
         enumerate_row<T, G, false>(r, terms, nterms, *win, sym_ins);
@@ -346,7 +350,7 @@ __global__ void __launch_bounds__(G == 32 ? 256 : G)
     k_num_hash(const uint32_t* __restrict__ list, uint32_t count,
                const TermDev<T>* terms, int nterms,
                const uint32_t* __restrict__ crp, uint32_t* __restrict__ cci,
-               T* __restrict__ cv, T ident_val, int key_bits) {
+               T* __restrict__ cv, T ident_val, int key_bits, int flat) {
   constexpr int RPB = G == 32 ? 8 : 1;
   constexpr int LOG2T = __builtin_ctz(TAB);
   extern __shared__ __align__(16) unsigned char smem[];
@@ -370,16 +374,22 @@ __global__ void __launch_bounds__(G == 32 ? 256 : G)
     }
     gsync<G>();
     auto num_ins = [&](uint32_t key, T v) {
+        // a plain load finds keys already present (most products of hot
+        // columns) without a CAS; only empty-looking slots are CAS-claimed
         uint32_t s = hslot(key, LOG2T);
         for (;;) {
-          const uint32_t old = atomicCAS(keys + s, kEmpty, key);
-          if (old == kEmpty || old == key) break;
+          const uint32_t cur = reinterpret_cast<volatile uint32_t*>(keys)[s];
+          if (cur == key) break;
+          if (cur == kEmpty) {
+            const uint32_t old = atomicCAS(keys + s, kEmpty, key);
+            if (old == kEmpty || old == key) break;
+          }
           s = (s + 1) & (TAB - 1);
         }
         atomicAdd(vals + s, v);
     };
     if (active) {
-      if constexpr (G >= 512)
+      if (G >= 512 && !flat)
         enumerate_row_warps<T, G, true>(r, terms, nterms, num_ins);
       else
         enumerate_row<T, G, true>(r, terms, nterms, *win, num_ins);
@@ -470,7 +480,7 @@ __global__ void __launch_bounds__(kDenseThreads)
                 const TermDev<T>* terms, int nterms,
                 const uint32_t* __restrict__ crp, uint32_t* __restrict__ cci,
                 T* __restrict__ cv, uint32_t* bitmaps, T* dense, uint32_t nwords,
-                uint32_t ncols, T ident_val) {
+                uint32_t ncols, T ident_val, int flat) {
   constexpr int G = kDenseThreads;
   constexpr int LOG2W = __builtin_ctz(kWc);
   namespace cg = cooperative_groups;
@@ -495,11 +505,10 @@ __global__ void __launch_bounds__(kDenseThreads)
   __syncthreads();
   for (uint32_t li = cid; li < count; li += ncl) {
     const uint32_t r = list[li];
-    enumerate_row_warps<T, G, true>(
-        r, terms, nterms,
-        [&](uint32_t key, T v) {
+    auto dense_ins = [&](uint32_t key, T v) {
           const uint32_t sl = hslot(key, LOG2W);
-          const uint32_t old = atomicCAS(wkey + sl, kEmpty, key);
+          const uint32_t cur = reinterpret_cast<volatile uint32_t*>(wkey)[sl];
+          const uint32_t old = cur == kEmpty ? atomicCAS(wkey + sl, kEmpty, key) : cur;
           if (old == key) {  // cached: its bit is already set
             atomicAdd(wval + sl, v);
             return;
@@ -510,8 +519,13 @@ __global__ void __launch_bounds__(kDenseThreads)
             atomicAdd(wval + sl, v);
           else
             atomicAdd(dv + key, v);
-        },
-        part, CL);
+        };
+    // flat: products spread over every thread of the CTA(s) by a block scan
+    // of the B-row lengths (balanced); otherwise whole A entries per warp
+    if (flat)
+      enumerate_row<T, G, true>(r, terms, nterms, win, dense_ins, part, CL);
+    else
+      enumerate_row_warps<T, G, true>(r, terms, nterms, dense_ins, part, CL);
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < kWc; i += G) {  // flush the cache
       const uint32_t key = wkey[i];
@@ -636,6 +650,14 @@ inline int dense_cl() {
   }();
   return v;
 }
+// RDMM_SPGEMM_FLAT=0|1: dense-tier product enumeration (dev switch).
+inline int dense_flat() {
+  static const int v = [] {
+    const char* e = std::getenv("RDMM_SPGEMM_FLAT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
 inline uint32_t dense_rows_in_flight(uint32_t rows, int cl) {
   return std::max<uint32_t>(1, std::min<uint32_t>(rows, uint32_t(num_sms()) / cl));
 }
@@ -662,7 +684,7 @@ int launch_dense_num(uint32_t slots, const uint32_t* list, uint32_t count,
   cfg.numAttrs = 1;
   count_launch();
   RDMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, list, count, td, nt, crp, cci, cv, bm, dense,
-                                   nwords, ncols, ident));
+                                   nwords, ncols, ident, dense_flat()));
   return RDMM_OK;
 }
 
@@ -708,7 +730,7 @@ int launch_sym_hash(const uint32_t* list, uint32_t count,
   const uint64_t blocks = std::min<uint64_t>(ceil_div(count, RPB),
                                              uint64_t(num_sms()) * 64);
   count_launch();
-  fn<<<unsigned(blocks), threads, sm, s>>>(list, count, terms, nterms, cnt64);
+  fn<<<unsigned(blocks), threads, sm, s>>>(list, count, terms, nterms, cnt64, dense_flat());
   return 0;
 }
 
@@ -728,7 +750,7 @@ int launch_num_hash(const uint32_t* list, uint32_t count,
                                              uint64_t(num_sms()) * 64);
   count_launch();
   fn<<<unsigned(blocks), threads, sm, s>>>(list, count, terms, nterms, crp,
-                                           cci, cv, ident, key_bits);
+                                           cci, cv, ident, key_bits, dense_flat());
   return 0;
 }
 
