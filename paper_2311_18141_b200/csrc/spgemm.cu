@@ -474,7 +474,10 @@ constexpr size_t dense_smem_bytes() {
   return size_t(kWc) * (4 + sizeof(T));
 }
 
-template <typename T, int CL>
+// SBM: the row's column bitmap lives in shared memory after the
+// write-combining cache (CL = 1 and ncols <= ~1M fp32): the bitmap atomics,
+// the count scan and the emission scan never touch HBM.
+template <typename T, int CL, bool SBM>
 __global__ void __launch_bounds__(kDenseThreads)
     k_dense_num(const uint32_t* __restrict__ list, uint32_t count,
                 const TermDev<T>* terms, int nterms,
@@ -492,7 +495,14 @@ __global__ void __launch_bounds__(kDenseThreads)
   __shared__ uint32_t slice_count;
   const uint32_t part = CL > 1 ? cluster.block_rank() : 0;
   const uint32_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
-  uint32_t* bm = bitmaps + size_t(cid) * nwords;
+  uint32_t* bm = SBM ? reinterpret_cast<uint32_t*>(dsm + dense_smem_bytes<T>())
+                     : bitmaps + size_t(cid) * nwords;
+  auto ldbm = [&](uint32_t w) -> uint32_t {
+    if constexpr (SBM) return reinterpret_cast<volatile uint32_t*>(bm)[w];
+    else return __ldcg(bm + w);
+  };
+  if constexpr (SBM)
+    for (uint32_t i = threadIdx.x; i < nwords; i += G) bm[i] = 0;
   T* dv = dense + size_t(cid) * ncols;
   const uint32_t wper = (nwords + CL - 1) / CL;
   const uint32_t ws0 = min(part * wper, nwords), ws1 = min(ws0 + wper, nwords);
@@ -514,7 +524,7 @@ __global__ void __launch_bounds__(kDenseThreads)
             return;
           }
           const uint32_t bit = 1u << (key & 31);
-          if (!(__ldcg(bm + (key >> 5)) & bit)) atomicOr(bm + (key >> 5), bit);
+          if (!(ldbm(key >> 5) & bit)) atomicOr(bm + (key >> 5), bit);
           if (old == kEmpty)
             atomicAdd(wval + sl, v);
           else
@@ -538,7 +548,7 @@ __global__ void __launch_bounds__(kDenseThreads)
     __threadfence();
     if constexpr (CL > 1) cluster.sync(); else __syncthreads();
     uint32_t c = 0;
-    for (uint32_t w = w0; w < w1; ++w) c += __popc(__ldcg(bm + w));
+    for (uint32_t w = w0; w < w1; ++w) c += __popc(ldbm(w));
     uint32_t total;
     const uint32_t off = gscan<G>(c, win.sums, total);
     uint32_t base = 0;
@@ -549,7 +559,7 @@ __global__ void __launch_bounds__(kDenseThreads)
     }
     uint32_t pos = crp[r] + base + off;
     for (uint32_t w = w0; w < w1; ++w) {
-      uint32_t bits = __ldcg(bm + w);
+      uint32_t bits = ldbm(w);
       if (!bits) continue;
       bm[w] = 0;
       while (bits) {
@@ -650,11 +660,16 @@ inline int dense_cl() {
   }();
   return v;
 }
-// RDMM_SPGEMM_FLAT=0|1: dense-tier product enumeration (dev switch).
+// Heavy-row product enumeration for the CTA tiers (G >= 512) and the dense
+// tier: 1 (default) = block-balanced flattened products (a block scan of the
+// B-row lengths per window of A entries); 0 = whole A entries per warp, which
+// leaves warps waiting at the row barrier behind R-MAT hub B rows (ncu:
+// barrier stalls 92 cycles/instr; s20 283 ms vs 207 ms).  RDMM_SPGEMM_FLAT
+// overrides (dev switch).
 inline int dense_flat() {
   static const int v = [] {
     const char* e = std::getenv("RDMM_SPGEMM_FLAT");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 1;
   }();
   return v;
 }
@@ -667,8 +682,11 @@ int launch_dense_num(uint32_t slots, const uint32_t* list, uint32_t count,
                      const TermDev<T>* td, int nt, const uint32_t* crp, uint32_t* cci, T* cv,
                      uint32_t* bm, T* dense, uint32_t nwords, uint32_t ncols, T ident,
                      cudaStream_t s) {
-  auto fn = k_dense_num<T, CL>;
-  const size_t sm = dense_smem_bytes<T>();
+  // static shared memory of the kernel: Win<T, G> + a counter
+  const size_t stat = sizeof(Win<T, kDenseThreads>) + 64;
+  const bool sbm = CL == 1 && dense_smem_bytes<T>() + size_t(nwords) * 4 + stat <= 226 * 1024;
+  auto fn = sbm ? k_dense_num<T, CL, true> : k_dense_num<T, CL, false>;
+  const size_t sm = dense_smem_bytes<T>() + (sbm ? size_t(nwords) * 4 : 0);
   RDMM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(slots * CL);
