@@ -328,6 +328,29 @@ class RankCtx {
 // a barrier return instead of deadlocking; the first error is rethrown.
 template <typename F>
 void run_ranks(Fabric& f, F&& fn) {
+  if (f.nlocal() == 1) {
+    // one rank in this process (one process per GPU): run it on the calling
+    // thread -- no thread start per collective call -- and restore the
+    // caller's current device afterwards
+    int prev = 0;
+    const bool have_prev = rdmm_get_device(&prev) == RDMM_OK;
+    const rank_t r = f.first_local();
+    try {
+      rdmm_set_device(f.device_of(r));
+      RankCtx ctx(f, r);
+      fn(ctx);
+    } catch (const std::exception& e) {
+      rdmm_fabric_abort(f.handle(), e.what());
+      if (have_prev) rdmm_set_device(prev);
+      throw;
+    } catch (...) {
+      rdmm_fabric_abort(f.handle(), "rank failed");
+      if (have_prev) rdmm_set_device(prev);
+      throw;
+    }
+    if (have_prev) rdmm_set_device(prev);
+    return;
+  }
   std::vector<std::thread> threads;
   std::mutex err_mu;
   std::exception_ptr first_error;

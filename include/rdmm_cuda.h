@@ -400,6 +400,7 @@ int rdmm_event_sync(void* event);
 void rdmm_event_destroy(void* event);
 int rdmm_stream_sync(rdmm_stream_t stream);
 int rdmm_set_device(int device);
+int rdmm_get_device(int* device);
 int rdmm_device_count(int* n);
 /* Strided 2-D copy (any direction), e.g. a dense tile out of a global array. */
 int rdmm_memcpy2d(void* dst, uint64_t dpitch, const void* src, uint64_t spitch,

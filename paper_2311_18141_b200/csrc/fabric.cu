@@ -1014,6 +1014,10 @@ extern "C" int rdmm_stream_sync(rdmm_stream_t stream) {
   RDMM_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
   return RDMM_OK;
 }
+extern "C" int rdmm_get_device(int* device) {
+  RDMM_CUDA_TRY(cudaGetDevice(device));
+  return RDMM_OK;
+}
 extern "C" int rdmm_set_device(int device) {
   RDMM_CUDA_TRY(cudaSetDevice(device));
   return RDMM_OK;
