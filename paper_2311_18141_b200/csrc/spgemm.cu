@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(G == 32 ? 256 : G)
 // only misses and the final flush reach the global array with atomics.
 // The symbolic pass keeps the whole bitmap in shared memory when it fits.
 constexpr int kWc = 8192;  // write-combining slots per CTA
-constexpr int kProbe = 4;  // slots probed per key
+constexpr int kProbe = 1;  // slots probed per key (4-way measured 24% slower on s20)
 
 template <typename T>
 constexpr size_t dense_smem_bytes() {
