@@ -468,7 +468,6 @@ __global__ void __launch_bounds__(G == 32 ? 256 : G)
 // only misses and the final flush reach the global array with atomics.
 // The symbolic pass keeps the whole bitmap in shared memory when it fits.
 constexpr int kWc = 8192;  // write-combining slots per CTA
-constexpr int kProbe = 1;  // slots probed per key (4-way measured 24% slower on s20)
 
 template <typename T>
 constexpr size_t dense_smem_bytes() {
@@ -517,35 +516,19 @@ __global__ void __launch_bounds__(kDenseThreads)
   for (uint32_t li = cid; li < count; li += ncl) {
     const uint32_t r = list[li];
     auto dense_ins = [&](uint32_t key, T v) {
-          // kProbe-way lookup: a hot column whose home slot a colder column
-          // claimed first still finds a slot (else every one of its
-          // products would miss to the global array)
-          const uint32_t h = hslot(key, LOG2W);
-#pragma unroll
-          for (int p = 0; p < kProbe; ++p) {
-            const uint32_t sl = (h + p) & (kWc - 1);
-            const uint32_t cur = reinterpret_cast<volatile uint32_t*>(wkey)[sl];
-            if (cur == key) {  // cached: its bit is set by the claimer
-              atomicAdd(wval + sl, v);
-              return;
-            }
-            if (cur == kEmpty) {
-              const uint32_t old = atomicCAS(wkey + sl, kEmpty, key);
-              if (old == key) {
-                atomicAdd(wval + sl, v);
-                return;
-              }
-              if (old == kEmpty) {
-                const uint32_t bit = 1u << (key & 31);
-                if (!(ldbm(key >> 5) & bit)) atomicOr(bm + (key >> 5), bit);
-                atomicAdd(wval + sl, v);
-                return;
-              }
-            }
+          const uint32_t sl = hslot(key, LOG2W);
+          const uint32_t cur = reinterpret_cast<volatile uint32_t*>(wkey)[sl];
+          const uint32_t old = cur == kEmpty ? atomicCAS(wkey + sl, kEmpty, key) : cur;
+          if (old == key) {  // cached: its bit is already set
+            atomicAdd(wval + sl, v);
+            return;
           }
           const uint32_t bit = 1u << (key & 31);
           if (!(ldbm(key >> 5) & bit)) atomicOr(bm + (key >> 5), bit);
-          atomicAdd(dv + key, v);
+          if (old == kEmpty)
+            atomicAdd(wval + sl, v);
+          else
+            atomicAdd(dv + key, v);
         };
     // flat: products spread over every thread of the CTA(s) by a block scan
     // of the B-row lengths (balanced); otherwise whole A entries per warp
