@@ -247,7 +247,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
         kn[j] = ok ? __ldcs(p.ci + idx) : 0u;
         an[j] = ok ? __ldcs(p.val + idx) : T(0);
       }
-#pragma unroll
+      // not unrolled: the row-flush code below would otherwise be inlined
+      // kWin times (instruction-cache misses showed up as no_instruction
+      // stalls in ncu)
+#pragma unroll 1
       for (int t = 0; t < kWin; t += kU) {
         if (t < int(cnt)) {
           V bv[kU][NV];
