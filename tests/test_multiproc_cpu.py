@@ -108,3 +108,21 @@ def test_bench_session_and_layout():
     (pr, pc), tiles = bench.layout(bench.CONFIGS["cfg4"], 4, A)
     assert (pr, pc) == (4, 1) and tiles[0] == (1 << 20) // 16
     assert bench.make_session(1, 0) is None
+
+
+def test_bench_owned_tile_bytes():
+    import bench
+
+    class G:
+        def __init__(self, pr, pc):
+            self.pr, self.pc = pr, pc
+
+        def owner(self, i, j):  # ProcGrid rule, distmat.hpp:20-36
+            return (i % self.pr) * self.pc + (j % self.pc)
+
+    # 10 x 6 fp32 in 4 x 4 tiles on a 2 x 1 grid: rank 0 owns tile rows 0 and 2
+    assert bench.owned_dense_bytes(G(2, 1), 10, 6, 4, 4, 0) == (4 + 2) * 6 * 4
+    assert bench.owned_dense_bytes(G(2, 1), 10, 6, 4, 4, 1) == 4 * 6 * 4
+    # every element is owned exactly once
+    g = G(2, 2)
+    assert sum(bench.owned_dense_bytes(g, 10, 6, 4, 4, r) for r in range(4)) == 10 * 6 * 4
