@@ -236,6 +236,7 @@ def run_ours(args, cfg, dev, rank, world):
     import paper_2311_18141_b200 as rd
     import paper_2311_18141_b200.dist as dm
     from paper_2311_18141_b200 import _lib as L
+    from paper_2311_18141_b200.analytics import imbalance_from_flops
 
     tdist = torch.distributed if world > 1 else None
     a, b = gen_inputs(cfg, dev)
@@ -303,7 +304,19 @@ def run_ours(args, cfg, dev, rank, world):
     kms, kcount = L.kernel_time(kind_id)
     L.rdmm_kernel_timing(0)
     ms_local = sum(per) / len(per)
-    imbalance = None
+    # per-rank per-k-step flops of the last timed run (RankStats::stage_flops);
+    # rows of ranks hosted by other processes are zero, so a SUM assembles it
+    sf = rep.stage_flops
+    width = torch.tensor([sf.shape[1]], device=dev, dtype=torch.int64)
+    if tdist:
+        tdist.all_reduce(width, op=tdist.ReduceOp.MAX)
+    table = torch.zeros((sf.shape[0], int(width[0])), device=dev, dtype=torch.float64)
+    table[:, :sf.shape[1]] = torch.as_tensor(sf, dtype=torch.float64)
+    if tdist:
+        tdist.all_reduce(table, op=tdist.ReduceOp.SUM)
+    stage_imb = imbalance_from_flops(table.cpu().numpy())
+    imbalance = {**stage_imb, "definition": "analytics.hpp:66-90 over the run's own "
+                 "per-rank per-k-step flop table"}
     if tdist:  # per-rank work and time, for the reference's imbalance metrics
         tt = torch.tensor([ms_local, float(flops_local)], device=dev, dtype=torch.float64)
         allt = [torch.zeros_like(tt) for _ in range(world)]
@@ -312,7 +325,7 @@ def run_ours(args, cfg, dev, rank, world):
         works = [float(x[1]) for x in allt]
         imbalance = {"time_max_over_avg": max(times) / (sum(times) / world),
                      "flops_max_over_avg": max(works) / max(1e-30, sum(works) / world),
-                     "per_rank_ms": times,
+                     "per_rank_ms": times, **stage_imb,
                      "definition": "max/avg over ranks (analytics.hpp:58-89 applied to "
                                    "per-rank device time and FlopMeter work)"}
     if tdist:  # max over ranks of the device time; flops summed over ranks

@@ -105,6 +105,11 @@ typedef struct {
   double total_seconds[RDMM_H_MAX_RANKS];
   uint64_t ntriples;     /* recorded (i,j,k) triples, all local ranks */
   uint32_t* triples;     /* 4 x uint32 per triple: rank, i, j, k (malloc'd) */
+  /* Per-rank flops per k tile step (RankStats::stage_flops, the table of
+   * analytics.hpp:66-90): nranks x nstages row-major, malloc'd (free with
+   * rdmm_h_free); ranks hosted by other processes are zero rows. */
+  uint32_t nstages;
+  uint64_t* stage_flops;
 } rdmm_h_report;
 
 int rdmm_h_run_multiply(rdmm_h_fabric* f, rdmm_h_matrix* A, rdmm_h_matrix* B,

@@ -158,6 +158,10 @@ class _Impl:
                                              C.c_void_p, P(C.c_uint64)])
             self._fn("spgemm_local", C.c_int, [P(OrcCsr), P(OrcCsr), P(OrcCsr), P(C.c_uint64)])
             self._fn("hardware_concurrency", C.c_uint, [])
+            self._fn("stage_imbalance", C.c_int, [P(OrcCsr), C.c_uint32, C.c_uint32]
+                     + [P(C.c_double)] * 3 + [C.c_void_p])
+            self._fn("imbalance_from_flops", None, [C.c_uint32, C.c_uint32, C.c_void_p,
+                                                    P(C.c_double), P(C.c_double)])
             self._fn("run_multiply_spmm", C.c_int,
                      [C.c_int] * 5 + [C.c_uint64, C.c_double, C.c_double, C.c_uint32, C.c_uint32]
                      + [C.c_uint64] * 3 + [C.c_uint32] * 3
@@ -275,6 +279,23 @@ class _Impl:
         o = OrcCsr()
         self._check(self._csr_add(C.byref(ao), C.byref(bo), C.byref(o)), "csr_add")
         return self._take(o)
+
+    def stage_imbalance(self, a: Csr, grid: int, stages: int = 0) -> dict:
+        ao, keep = as_orc(a)
+        K = stages or grid
+        fl = np.zeros((grid * grid, K), np.uint64)
+        ps, e2e, nb = C.c_double(), C.c_double(), C.c_double()
+        self._check(self._stage_imbalance(C.byref(ao), grid, stages, C.byref(ps), C.byref(e2e),
+                                          C.byref(nb), fl.ctypes.data), "stage_imbalance")
+        return {"per_stage_flop_imbalance": ps.value, "end_to_end_flop_imbalance": e2e.value,
+                "nnz_imbalance": nb.value, "stage_flops": fl.astype(np.int64)}
+
+    def imbalance_from_flops(self, f: np.ndarray) -> dict:
+        f = np.ascontiguousarray(f, np.uint64)
+        ps, e2e = C.c_double(), C.c_double()
+        self._imbalance_from_flops(f.shape[0], f.shape[1], f.ctypes.data, C.byref(ps),
+                                   C.byref(e2e))
+        return {"per_stage_flop_imbalance": ps.value, "end_to_end_flop_imbalance": e2e.value}
 
     def checksum_dense(self, g: np.ndarray, tm: int, tn: int) -> float:
         return float(self._checksum_dense(g.shape[0], g.shape[1], tm, tn, g.ctypes.data,

@@ -14,6 +14,7 @@
 #include <thread>
 
 #include "rdmm/algos.hpp"
+#include "rdmm/analytics.hpp"
 #include "rdmm/gen.hpp"
 #include "rdmm_oracle.h"  // orc_csr layout only
 
@@ -234,6 +235,37 @@ int ref_csr_add(const orc_csr* a, const orc_csr* b, orc_csr* out) {
   } catch (...) {
     return code_of(std::current_exception());
   }
+}
+
+// analytics.hpp:97-150 on the reference's own host tile; stage_flops is
+// caller-owned [grid*grid, stages or grid].
+int ref_stage_imbalance(const orc_csr* a, uint32_t grid, uint32_t stages, double* per_stage,
+                        double* end_to_end, double* nnz_imb, uint64_t* stage_flops) {
+  try {
+    auto rep = a->dtype == 8 ? stage_imbalance(tile_of<double>(a), grid, stages)
+                             : stage_imbalance(tile_of<float>(a), grid, stages);
+    *per_stage = rep.per_stage_flop_imbalance;
+    *end_to_end = rep.end_to_end_flop_imbalance;
+    *nnz_imb = rep.nnz_imbalance;
+    std::size_t q = 0;
+    for (auto& r : rep.stage_flops)
+      for (auto v : r) stage_flops[q++] = v;
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+// analytics.hpp:66-90 on a [P, S] row-major flop table.
+void ref_imbalance_from_flops(uint32_t P, uint32_t S, const uint64_t* f, double* per_stage,
+                              double* end_to_end) {
+  ImbalanceReport rep;
+  rep.stage_flops.assign(P, std::vector<std::uint64_t>(S, 0));
+  for (uint32_t r = 0; r < P; ++r)
+    for (uint32_t s = 0; s < S; ++s) rep.stage_flops[r][s] = f[std::size_t(r) * S + s];
+  imbalance_from_flops(rep);
+  *per_stage = rep.per_stage_flop_imbalance;
+  *end_to_end = rep.end_to_end_flop_imbalance;
 }
 
 void ref_csr_free(orc_csr* a) {

@@ -1,5 +1,6 @@
 // host_capi.cpp -- C-ABI over the C++ driver layer (include/rdmm/*.hpp),
 // see include/rdmm_host.h.
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
@@ -8,6 +9,7 @@
 #include <variant>
 
 #include "rdmm/algos.hpp"
+#include "rdmm/analytics.hpp"
 #include "rdmm_host.h"
 
 using namespace rdmm;
@@ -122,6 +124,16 @@ void fill(const RunReport& r, rdmm_h_report* out) {
     out->bytes_on_node[p] = s.bytes_on_node;
     out->bytes_off_node[p] = s.bytes_off_node;
     out->total_seconds[p] = s.total_seconds;
+  }
+  std::size_t ns = 0;
+  for (auto& s : r.per_rank) ns = std::max(ns, s.stage_flops.size());
+  out->nstages = uint32_t(ns);
+  if (ns && !r.per_rank.empty()) {
+    out->stage_flops =
+        static_cast<uint64_t*>(std::calloc(r.per_rank.size() * ns, sizeof(uint64_t)));
+    for (std::size_t p = 0; p < r.per_rank.size(); ++p)
+      std::copy(r.per_rank[p].stage_flops.begin(), r.per_rank[p].stage_flops.end(),
+                out->stage_flops + p * ns);
   }
   out->ntriples = nt;
   if (nt) {

@@ -37,7 +37,8 @@ class Report(C.Structure):
                                          "steals_local", "pushes", "pops", "bytes_self",
                                          "bytes_on_node", "bytes_off_node")] + [
         ("total_seconds", C.c_double * MAXR), ("ntriples", C.c_uint64),
-        ("triples", C.POINTER(C.c_uint32))]
+        ("triples", C.POINTER(C.c_uint32)), ("nstages", C.c_uint32),
+        ("stage_flops", C.POINTER(C.c_uint64))]
 
 
 _u32, _u64, _vp, _int = C.c_uint32, C.c_uint64, C.c_void_p, C.c_int
@@ -275,6 +276,14 @@ class RunReport:
     total_steals: int
     per_rank: list = field(default_factory=list)
     triples: list = field(default_factory=list)
+    # flops per rank per k tile step (RankStats::stage_flops), int64 [P, K]
+    stage_flops: np.ndarray = field(default_factory=lambda: np.zeros((0, 0), np.int64))
+
+    def imbalance(self):
+        """Per-stage and end-to-end flop imbalance of this run
+        (analytics.hpp:66-90 over the multiply's own flop table)."""
+        from .analytics import imbalance_from_flops
+        return imbalance_from_flops(self.stage_flops)
 
 
 def run_multiply(f: Fabric, A: DistSparse, B, Cm, variant="stationary_c", ws_base="stationary_a",
@@ -302,5 +311,10 @@ def run_multiply(f: Fabric, A: DistSparse, B, Cm, variant="stationary_c", ws_bas
         a = np.ctypeslib.as_array(r.triples, shape=(r.ntriples * 4,)).reshape(-1, 4).copy()
         tr = [tuple(int(x) for x in row) for row in a]
         _h.rdmm_h_free(r.triples)
+    sf = np.zeros((r.nranks, r.nstages), np.int64)
+    if r.nstages and r.stage_flops:
+        sf[:] = np.ctypeslib.as_array(r.stage_flops, shape=(r.nranks * r.nstages,)).reshape(
+            r.nranks, r.nstages)
+        _h.rdmm_h_free(r.stage_flops)
     return RunReport(r.wall_seconds, r.checksum, r.total_flops, r.total_multiplies,
-                     r.total_steals, per, tr)
+                     r.total_steals, per, tr, sf)

@@ -99,6 +99,19 @@ def main():
         assert np.array_equal(c.values, outs[0][0].values) and cs == outs[0][1]
     csr(g, "algo_spgemm", outs[0][0])
     g["algo_spgemm_checksum"] = np.array([outs[0][1]])
+    # analytics.hpp:66-150: predicted stage imbalance of A*A and the flop-table reduction
+    a10 = R.rmat(10, 8, seed=1)
+    for grid, stages in ((2, 0), (2, 4), (3, 6)):
+        r = R.stage_imbalance(a10, grid, stages)
+        key = f"stage_g{grid}s{stages}"
+        g[key + "_flops"] = r["stage_flops"]
+        g[key + "_imb"] = np.array([r["per_stage_flop_imbalance"],
+                                    r["end_to_end_flop_imbalance"], r["nnz_imbalance"]])
+    tab = np.random.default_rng(5).integers(0, 1000, size=(5, 7)).astype(np.uint64)
+    tab[2] = 0
+    g["imb_table"] = tab.astype(np.int64)
+    r = R.imbalance_from_flops(tab)
+    g["imb_table_out"] = np.array([r["per_stage_flop_imbalance"], r["end_to_end_flop_imbalance"]])
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(path, **g)
     print("wrote", path, os.path.getsize(path), "bytes")

@@ -304,3 +304,36 @@ def test_rmat_distributed_spmm_device_init(dist):
             Cm.init()
             dist.run_multiply(f, A, B, Cm, variant=v, ws_base="stationary_c")
             assert np.array_equal(Cm.to_global(), want.cpu().numpy()), v
+
+
+@pytest.mark.parametrize("tile,key", [(512, "stage_g2s0"), (256, "stage_g2s4")])
+def test_run_stage_flops_match_reference_stage_imbalance(dist, orc, golden, tile, key):
+    """The per-rank per-k-step flop table recorded by a stationary-C SpGEMM
+    A*A on a 2x2 grid equals the reference's predicted table
+    (analytics.hpp:97-150, golden from the unmodified reference), and so do
+    the per-stage / end-to-end imbalance figures derived from it."""
+    rp, ci = golden["rmat10_rp"], golden["rmat10_ci"]
+    n = len(rp) - 1
+    vv = golden["rmat10_v"].astype(np.float64)
+    g = dist.ProcGrid(2, 2)
+    with fabric(dist, 4, 32 << 20) as f:
+        A = dist.DistSparse(f, n, n, tile, tile, g, 0, dtype=np.float64)
+        B = dist.DistSparse(f, n, n, tile, tile, g, 1, dtype=np.float64)
+        Cm = dist.DistSparse(f, n, n, tile, tile, g, 2, dtype=np.float64)
+        A.init_from_global(rp, ci, vv)
+        B.init_from_global(rp, ci, vv)
+        Cm.init()
+        rep = dist.run_multiply(f, A, B, Cm, variant="stationary_c")
+    assert np.array_equal(rep.stage_flops, golden[key + "_flops"])
+    assert [int(x) for x in rep.stage_flops.sum(axis=1)] == [p["flops"] for p in rep.per_rank]
+    imb = rep.imbalance()
+    np.testing.assert_allclose([imb["per_stage_flop_imbalance"], imb["end_to_end_flop_imbalance"]],
+                               golden[key + "_imb"][:2], rtol=1e-12)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_stage_flops_cover_every_multiply(dist, orc, variant):
+    got, want, rep = run_spmm(dist, orc, variant=variant)
+    assert rep.stage_flops.shape[0] == 4
+    assert int(rep.stage_flops.sum()) == rep.total_flops
+    assert [int(x) for x in rep.stage_flops.sum(axis=1)] == [p["flops"] for p in rep.per_rank]
