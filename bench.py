@@ -440,6 +440,22 @@ def run_ours(args, cfg, dev, rank, world):
     }
     if imbalance:
         out["imbalance"] = imbalance
+    # the paper's roofline model (model.hpp:139-160) with B200 costs: local
+    # HBM bound and NVLink inter-GPU bound for this shape at N GPUs
+    from paper_2311_18141_b200 import model as md
+    try:
+        shp = md.ProblemShape(m, k, n, world, nnz_a / (float(m) * k), 4)
+        mod = md.roofline(shp, md.CostModel(mem_bw=hbm * 1e9), cfg["kind"], total_flops,
+                          out_nnz or 0)
+        out["model"] = {"local_peak_gflops": mod["local_peak"] / 1e9,
+                        "internode_bound_gflops": mod["internode_bound"] * world / 1e9,
+                        "bound_kind": mod["bound_kind"], "local_ai": mod["local_ai"],
+                        "internode_ai": mod["internode_ai"],
+                        "value_over_bound": out["value"] / (mod["internode_bound"] * world / 1e9),
+                        "source": "model.hpp:139-160, B200 CostModel (NVLink 900 GB/s, "
+                                  "measured HBM, fp32 FMA peak); bound x n_gpus"}
+    except ValueError as e:
+        out["model"] = {"unavailable": str(e)}
     if out_nnz is not None:
         out["config"]["nnz_out"] = out_nnz
     f.close()

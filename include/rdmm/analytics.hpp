@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "algos.hpp"
+#include "model.hpp"  // CostModel
 
 namespace rdmm {
 
@@ -26,23 +27,6 @@ struct ImbalanceReport {  // analytics.hpp:18-25
   std::vector<std::vector<std::uint64_t>> stage_flops;  // [rank][stage]
   double per_stage_flop_imbalance = 1.0;
   double end_to_end_flop_imbalance = 1.0;
-};
-
-// Cost parameters of virtual_time (model.hpp:16-31).  Defaults describe one
-// B200 box: NVLink 5 peer bandwidth for both intra and "network" transfers,
-// HBM3e as local memory, fp32 CUDA-core FMA peak as arithmetic.
-struct CostModel {
-  double net_bw = 900e9;
-  double intra_bw = 900e9;
-  double mem_bw = 6446.3e9;
-  double arith_peak = 74e12;
-  double w = 4;
-  double latency = 0;
-  void validate() const {
-    if (!(net_bw > 0 && intra_bw > 0 && mem_bw > 0 && arith_peak > 0) || latency < 0)
-      throw std::invalid_argument("cost model parameters must be positive");
-    if (w != 4 && w != 8) throw std::invalid_argument("word size must be 4 or 8 bytes");
-  }
 };
 
 namespace analytics_detail {

@@ -160,6 +160,8 @@ class _Impl:
             self._fn("hardware_concurrency", C.c_uint, [])
             self._fn("stage_imbalance", C.c_int, [P(OrcCsr), C.c_uint32, C.c_uint32]
                      + [P(C.c_double)] * 3 + [C.c_void_p])
+            self._fn("roofline", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_uint64,
+                                           C.c_uint64, C.c_void_p])
             self._fn("imbalance_from_flops", None, [C.c_uint32, C.c_uint32, C.c_void_p,
                                                     P(C.c_double), P(C.c_double)])
             self._fn("run_multiply_spmm", C.c_int,
@@ -296,6 +298,14 @@ class _Impl:
         self._imbalance_from_flops(f.shape[0], f.shape[1], f.ctypes.data, C.byref(ps),
                                    C.byref(e2e))
         return {"per_stage_flop_imbalance": ps.value, "end_to_end_flop_imbalance": e2e.value}
+
+    def roofline(self, shape, cost, spgemm=False, flops=0, out_nnz=0) -> np.ndarray:
+        sh = np.asarray(shape, np.float64)
+        co = np.asarray(cost, np.float64)
+        out = np.zeros(7)
+        self._check(self._roofline(sh.ctypes.data, co.ctypes.data, int(spgemm), flops, out_nnz,
+                                   out.ctypes.data), "roofline")
+        return out
 
     def checksum_dense(self, g: np.ndarray, tm: int, tn: int) -> float:
         return float(self._checksum_dense(g.shape[0], g.shape[1], tm, tn, g.ctypes.data,

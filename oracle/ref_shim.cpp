@@ -15,6 +15,7 @@
 
 #include "rdmm/algos.hpp"
 #include "rdmm/analytics.hpp"
+#include "rdmm/model.hpp"
 #include "rdmm/gen.hpp"
 #include "rdmm_oracle.h"  // orc_csr layout only
 
@@ -266,6 +267,31 @@ void ref_imbalance_from_flops(uint32_t P, uint32_t S, const uint64_t* f, double*
   imbalance_from_flops(rep);
   *per_stage = rep.per_stage_flop_imbalance;
   *end_to_end = rep.end_to_end_flop_imbalance;
+}
+
+// model.hpp:139-160 roofline (+ comm volume, -1 when p is not square).
+// shape = {m, k, n, p, d, w}; cost = {net_bw, intra_bw, mem_bw, arith_peak};
+// out = {local_ai, internode_ai, local_peak, internode_bound, bound_kind,
+//        comm_elems_per_iter, comm_bytes_per_iter(idx 4)}.
+int ref_roofline(const double* shape, const double* cost, int spgemm, uint64_t flops,
+                 uint64_t out_nnz, double* out) {
+  try {
+    ProblemShape s;
+    s.m = shape[0]; s.k = shape[1]; s.n = shape[2]; s.p = shape[3]; s.d = shape[4]; s.w = shape[5];
+    CostModel c;
+    c.net_bw = cost[0]; c.intra_bw = cost[1]; c.mem_bw = cost[2]; c.arith_peak = cost[3];
+    c.w = s.w;
+    std::optional<FlopMeter> m;
+    if (spgemm) m = FlopMeter{flops, out_nnz};
+    auto r = roofline(s, c, spgemm ? MultiplyKind::spgemm : MultiplyKind::spmm, m);
+    out[0] = r.local_ai; out[1] = r.internode_ai; out[2] = r.local_peak;
+    out[3] = r.internode_bound; out[4] = r.bound_kind == BoundKind::network_bound ? 0 : 1;
+    out[5] = s.p_square() ? comm_elems_per_iter(s) : -1.0;
+    out[6] = comm_bytes_per_iter(s, 4.0);
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
 }
 
 void ref_csr_free(orc_csr* a) {

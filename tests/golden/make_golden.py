@@ -17,6 +17,15 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 import oracle  # noqa: E402
 
 VARIANTS = list(oracle.VARIANTS)
+# (m, k, n, p, d, w, spgemm, flops, out_nnz): cfg3 SpMM at 1/4 GPUs, cfg5 at 2,
+# a fp64 case, cfg4 SpGEMM at 8 (survey-measured flops / output nnz)
+MODEL_CASES = [(4194304, 4194304, 128, 1, 64827941 / 4194304**2, 4, 0, 0, 0),
+               (4194304, 4194304, 128, 4, 64827941 / 4194304**2, 4, 0, 0, 0),
+               (4194304, 4194304, 256, 2, 16 / 4194304, 4, 0, 0, 0),
+               (65536, 65536, 128, 9, 490332 / 65536**2, 8, 0, 0, 0),
+               (1048576, 1048576, 1048576, 8, 8124707 / 1048576**2, 4, 1, 4696097190,
+                1390953199)]
+MODEL_COST = [900e9, 900e9, 6446.3e9, 74.4e12]
 
 
 def csr(out, name, c):
@@ -112,6 +121,11 @@ def main():
     g["imb_table"] = tab.astype(np.int64)
     r = R.imbalance_from_flops(tab)
     g["imb_table_out"] = np.array([r["per_stage_flop_imbalance"], r["end_to_end_flop_imbalance"]])
+    # model.hpp:139-160 roofline at the BASELINE configs' shapes with B200 costs
+    rows = []
+    for m, k, n, p, d, w, sg, fl, on in MODEL_CASES:
+        rows.append(R.roofline([m, k, n, p, d, w], MODEL_COST, sg, fl, on))
+    g["model_out"] = np.array(rows)
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(path, **g)
     print("wrote", path, os.path.getsize(path), "bytes")

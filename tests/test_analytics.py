@@ -51,11 +51,12 @@ def test_imbalance_edge_cases():
     assert an.nnz_imbalance([0, 1, 2], [0, 1], 2, 2, 2, 2) == pytest.approx(2.0)
 
 
-def test_cpp_analytics_header_compiles(tmp_path):
+def test_cpp_analytics_header_compiles(tmp_path, golden):
     # the C++ drop-in header (include/rdmm/analytics.hpp) on a host tile
     src = tmp_path / "t.cpp"
     src.write_text(r'''
 #include "rdmm/analytics.hpp"
+#include "rdmm/model.hpp"
 #include <cstdio>
 int main() {
   rdmm::CsrTile<float> a(4, 4);
@@ -64,8 +65,11 @@ int main() {
   rdmm::RunReport run; run.per_rank.resize(2);
   run.per_rank[0].stage_flops = {4, 4}; run.per_rank[1].stage_flops = {4};
   auto q = rdmm::run_imbalance(run);
-  std::printf("%.6f %.6f %.6f\n", r.nnz_imbalance, q.per_stage_flop_imbalance,
-              q.end_to_end_flop_imbalance);
+  rdmm::ProblemShape s; s.m = 4194304; s.k = 4194304; s.n = 128; s.p = 4;
+  s.d = 64827941.0 / (4194304.0 * 4194304.0);
+  auto rf = rdmm::roofline(s, rdmm::CostModel{}, rdmm::MultiplyKind::spmm);
+  std::printf("%.6f %.6f %.6f %.9e\n", r.nnz_imbalance, q.per_stage_flop_imbalance,
+              q.end_to_end_flop_imbalance, rf.internode_bound);
 }
 ''')
     exe = tmp_path / "t"
@@ -80,3 +84,32 @@ int main() {
     assert float(out[0]) == pytest.approx(a_blocks.max() / a_blocks.mean(), rel=1e-6)
     assert float(out[1]) == pytest.approx(8 / 6, rel=1e-6)
     assert float(out[2]) == pytest.approx(8 / 6, rel=1e-6)
+    assert float(out[3]) == pytest.approx(golden["model_out"][1][3], rel=1e-8)
+
+
+def test_model_roofline_matches_reference(golden):
+    """model.hpp:83-160 (reference) vs paper_2311_18141_b200.model at the
+    BASELINE configs' shapes with B200 costs (goldens from the reference)."""
+    import sys
+
+    from paper_2311_18141_b200 import model as md
+
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    from make_golden import MODEL_CASES, MODEL_COST
+
+    for case, want in zip(MODEL_CASES, golden["model_out"]):
+        m, k, n, p, d, w, sg, fl, on = case
+        s = md.ProblemShape(m, k, n, p, d, w)
+        c = md.CostModel(*MODEL_COST, w=w)
+        r = md.roofline(s, c, "spgemm" if sg else "spmm", fl, on)
+        got = [r["local_ai"], r["internode_ai"], r["local_peak"], r["internode_bound"],
+               0.0 if r["bound_kind"] == "network_bound" else 1.0,
+               md.comm_elems_per_iter(s) if s.p_square() else -1.0,
+               md.comm_bytes_per_iter(s, 4.0)]
+        np.testing.assert_allclose(got, want, rtol=1e-12)
+    with pytest.raises(ValueError):
+        md.comm_elems_per_iter(md.ProblemShape(8, 8, 8, 2, 0.5))
+    with pytest.raises(ValueError):
+        md.roofline(md.ProblemShape(8, 8, 8, 4, 0.5), kind="spgemm")
+    with pytest.raises(ValueError):
+        md.ProblemShape(8, 8, 8, 4, 1.5).validate()
