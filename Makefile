@@ -29,7 +29,7 @@ $(OBJ)/%.cpp.o: $(SRC)/%.cpp $(HDRS)
 
 $(LIBDIR)/librdmm_cuda.so: $(CUDA_OBJS) $(CXX_OBJS)
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(CUDA_OBJS) $(CXX_OBJS) -lpthread -lrt -ldl
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(CUDA_OBJS) $(CXX_OBJS) -lpthread -lrt -ldl -lz
 
 # C++ drop-in API test program (run on the GPU by tests/test_cpp_gpu.py)
 build/tests/test_api: tests/cpp/test_api.cpp $(LIBDIR)/librdmm_cuda.so $(HDRS)

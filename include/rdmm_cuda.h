@@ -44,7 +44,8 @@ typedef enum {
   RDMM_ERR_QUEUE_FULL = 4,     /* queue_full_error       fabric.hpp:55-60 */
   RDMM_ERR_PROTOCOL = 5,       /* protocol_error         algos.hpp:98-101 */
   RDMM_ERR_CUDA = 6,           /* CUDA runtime failure */
-  RDMM_ERR_INVALID = 7         /* std::invalid_argument / bad parameters */
+  RDMM_ERR_INVALID = 7,        /* std::invalid_argument / bad parameters */
+  RDMM_ERR_IO = 8              /* mmio_error             mmio.hpp:19-22 */
 } rdmm_status;
 
 /* Message of the last failure on the calling thread ("" if none). */

@@ -117,6 +117,17 @@ int rdmm_h_run_multiply(rdmm_h_fabric* f, rdmm_h_matrix* A, rdmm_h_matrix* B,
                         rdmm_h_report* rep);
 void rdmm_h_free(void* p);
 
+/* Matrix Market coordinate I/O (replaces rdmm::read_matrix_market /
+ * write_matrix_market, mmio.hpp:50-116): plain or gzip input; symmetric
+ * files expanded; duplicates summed.  Host CSR arrays are malloc'd (free with
+ * rdmm_h_free); dtype_bytes 4 (float) or 8 (double). */
+int rdmm_h_read_matrix_market(const char* path, int dtype_bytes, uint32_t* rows,
+                              uint32_t* cols, uint64_t* nnz, uint32_t** row_ptr,
+                              uint32_t** col_idx, void** values);
+int rdmm_h_write_matrix_market(const char* path, int dtype_bytes, uint32_t rows, uint32_t cols,
+                               const uint32_t* row_ptr, const uint32_t* col_idx,
+                               const void* values);
+
 #ifdef __cplusplus
 }
 #endif

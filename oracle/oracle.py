@@ -160,6 +160,8 @@ class _Impl:
             self._fn("hardware_concurrency", C.c_uint, [])
             self._fn("stage_imbalance", C.c_int, [P(OrcCsr), C.c_uint32, C.c_uint32]
                      + [P(C.c_double)] * 3 + [C.c_void_p])
+            self._fn("read_matrix_market", C.c_int, [C.c_char_p, C.c_int, P(OrcCsr),
+                                                     C.c_char_p, C.c_int])
             self._fn("roofline", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_uint64,
                                            C.c_uint64, C.c_void_p])
             self._fn("imbalance_from_flops", None, [C.c_uint32, C.c_uint32, C.c_void_p,
@@ -298,6 +300,17 @@ class _Impl:
         self._imbalance_from_flops(f.shape[0], f.shape[1], f.ctypes.data, C.byref(ps),
                                    C.byref(e2e))
         return {"per_stage_flop_imbalance": ps.value, "end_to_end_flop_imbalance": e2e.value}
+
+    def read_matrix_market(self, path: str, dtype=np.float32):
+        """-> Csr, or raises ValueError(message) on the reference's mmio_error."""
+        o = OrcCsr()
+        msg = C.create_string_buffer(512)
+        rc = self._read_matrix_market(str(path).encode(), np.dtype(dtype).itemsize, C.byref(o),
+                                      msg, 512)
+        if rc == 8:
+            raise ValueError(msg.value.decode())
+        self._check(rc, "read_matrix_market")
+        return self._take(o)
 
     def roofline(self, shape, cost, spgemm=False, flops=0, out_nnz=0) -> np.ndarray:
         sh = np.asarray(shape, np.float64)

@@ -7,6 +7,7 @@
 // generators / run_multiply (reference: proj/include/rdmm/{tile,gen,algos}.hpp)
 // on caller-owned host buffers.
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -16,6 +17,7 @@
 #include "rdmm/algos.hpp"
 #include "rdmm/analytics.hpp"
 #include "rdmm/model.hpp"
+#include "rdmm/mmio.hpp"
 #include "rdmm/gen.hpp"
 #include "rdmm_oracle.h"  // orc_csr layout only
 
@@ -289,6 +291,22 @@ int ref_roofline(const double* shape, const double* cost, int spgemm, uint64_t f
     out[5] = s.p_square() ? comm_elems_per_iter(s) : -1.0;
     out[6] = comm_bytes_per_iter(s, 4.0);
     return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+// mmio.hpp:50-101: 0 on success, 8 on mmio_error (message to stderr-free buffer)
+int ref_read_matrix_market(const char* path, int dtype, orc_csr* out, char* msg, int cap) {
+  try {
+    if (dtype == 8)
+      export_csr(read_matrix_market<double>(path), out);
+    else
+      export_csr(read_matrix_market<float>(path), out);
+    return 0;
+  } catch (const mmio_error& e) {
+    std::snprintf(msg, std::size_t(cap), "%s", e.what());
+    return 8;
   } catch (...) {
     return code_of(std::current_exception());
   }

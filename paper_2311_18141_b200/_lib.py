@@ -46,8 +46,13 @@ class InvalidArgument(RdmmError, ValueError):
     code = 7
 
 
+class MmioError(RdmmError):  # mmio.hpp:19-22
+    code = 8
+
+
 _ERRORS = {c.code: c for c in (DimensionError, FabricError, HeapExhaustedError,
-                               QueueFullError, ProtocolError, CudaError, InvalidArgument)}
+                               QueueFullError, ProtocolError, CudaError, InvalidArgument,
+                               MmioError)}
 
 
 def _load() -> C.CDLL:

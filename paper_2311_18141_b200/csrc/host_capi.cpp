@@ -10,6 +10,7 @@
 
 #include "rdmm/algos.hpp"
 #include "rdmm/analytics.hpp"
+#include "rdmm/mmio.hpp"
 #include "rdmm_host.h"
 
 using namespace rdmm;
@@ -30,6 +31,7 @@ namespace {
 
 int to_code(const std::exception& e) {
   std::string msg = e.what();
+  if (dynamic_cast<const mmio_error*>(&e)) return rdmm_impl_fail(RDMM_ERR_IO, msg.c_str());
   if (dynamic_cast<const dimension_error*>(&e)) return rdmm_impl_fail(RDMM_ERR_DIMENSION, msg.c_str());
   if (dynamic_cast<const heap_exhausted_error*>(&e)) return rdmm_impl_fail(RDMM_ERR_HEAP_EXHAUSTED, msg.c_str());
   if (dynamic_cast<const queue_full_error*>(&e)) return rdmm_impl_fail(RDMM_ERR_QUEUE_FULL, msg.c_str());
@@ -357,4 +359,62 @@ extern "C" int rdmm_h_sparse_owned_to_host(rdmm_h_matrix* mat, void* buf, uint64
 
 extern "C" void* rdmm_h_fabric_stream(rdmm_h_fabric* f, uint32_t rank) {
   return rdmm_fabric_stream(f->f->handle(), rank, 0);
+}
+
+namespace {
+template <typename T>
+void mm_read(const char* path, uint32_t* rows, uint32_t* cols, uint64_t* nnz, uint32_t** rp,
+             uint32_t** ci, void** vals) {
+  CsrTile<T> t = read_matrix_market<T>(path);
+  *rows = t.rows;
+  *cols = t.cols;
+  *nnz = t.col_idx.size();
+  auto dup = [](const auto& v) {
+    using E = typename std::decay_t<decltype(v)>::value_type;
+    E* p = static_cast<E*>(std::malloc(std::max<std::size_t>(1, v.size()) * sizeof(E)));
+    if (!p) throw std::bad_alloc();
+    std::copy(v.begin(), v.end(), p);
+    return p;
+  };
+  *rp = dup(t.row_ptr);
+  *ci = dup(t.col_idx);
+  *vals = dup(t.values);
+}
+
+template <typename T>
+void mm_write(const char* path, uint32_t rows, uint32_t cols, const uint32_t* rp,
+              const uint32_t* ci, const void* vals) {
+  CsrTile<T> t(rows, cols);
+  t.row_ptr.assign(rp, rp + rows + 1);
+  t.col_idx.assign(ci, ci + rp[rows]);
+  const T* v = static_cast<const T*>(vals);
+  t.values.assign(v, v + rp[rows]);
+  write_matrix_market(t, path);
+}
+}  // namespace
+
+extern "C" int rdmm_h_read_matrix_market(const char* path, int dtype_bytes, uint32_t* rows,
+                                         uint32_t* cols, uint64_t* nnz, uint32_t** row_ptr,
+                                         uint32_t** col_idx, void** values) {
+  return guarded([&] {
+    if (dtype_bytes == 8)
+      mm_read<double>(path, rows, cols, nnz, row_ptr, col_idx, values);
+    else if (dtype_bytes == 4)
+      mm_read<float>(path, rows, cols, nnz, row_ptr, col_idx, values);
+    else
+      throw std::invalid_argument("dtype_bytes must be 4 or 8");
+  });
+}
+
+extern "C" int rdmm_h_write_matrix_market(const char* path, int dtype_bytes, uint32_t rows,
+                                          uint32_t cols, const uint32_t* row_ptr,
+                                          const uint32_t* col_idx, const void* values) {
+  return guarded([&] {
+    if (dtype_bytes == 8)
+      mm_write<double>(path, rows, cols, row_ptr, col_idx, values);
+    else if (dtype_bytes == 4)
+      mm_write<float>(path, rows, cols, row_ptr, col_idx, values);
+    else
+      throw std::invalid_argument("dtype_bytes must be 4 or 8");
+  });
 }
