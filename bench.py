@@ -173,7 +173,7 @@ def owned_dense_bytes(grid, rows, cols, tr, tc, rank):
     return tot
 
 
-def gen_inputs(cfg, dev):
+def gen_inputs(cfg, dev, permute=0):
     import paper_2311_18141_b200 as rd
     import torch
 
@@ -182,6 +182,8 @@ def gen_inputs(cfg, dev):
     else:
         n = 1 << cfg["scale"]
         a = rd.uniform_tiles(n, n, 1, cfg["d"], 1, device=dev)
+    if permute:  # gen.hpp:134-155 symmetric relabelling (not the BASELINE default)
+        a = rd.permute_symmetric(a, permute)
     b = rd.random_dense(a.cols, cfg["n"], 2, device=dev) if cfg["kind"] == "spmm" else None
     torch.cuda.synchronize()
     return a, b
@@ -239,7 +241,7 @@ def run_ours(args, cfg, dev, rank, world):
     from paper_2311_18141_b200.analytics import imbalance_from_flops
 
     tdist = torch.distributed if world > 1 else None
-    a, b = gen_inputs(cfg, dev)
+    a, b = gen_inputs(cfg, dev, args.permute)
     m, k, nnz_a = a.rows, a.cols, a.nnz
     rp_host = a.row_ptr.cpu().numpy().view("uint32")
     n = cfg["n"] if cfg["kind"] == "spmm" else a.cols
@@ -424,7 +426,8 @@ def run_ours(args, cfg, dev, rank, world):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (reference generators, seeds A=1 B=2, built on device)",
-        "config": {"workload": args.config, "desc": cfg["desc"], "rows": m, "cols": k, "n": n,
+        "config": {"workload": args.config, "desc": cfg["desc"], "permute_seed": args.permute,
+                   "rows": m, "cols": k, "n": n,
                    "nnz": nnz_a, "flop_per_step": total_flops,
                    "variant": variant, "fuse_k": not args.no_fuse, "split_local": not args.no_split, "lookahead": args.lookahead, "grid": f"{pr}x{pc}", "tiles": [tm, tk, tn],
                    "path": "run_multiply (host C-ABI rdmm_h_run_multiply) over the fabric",
@@ -670,6 +673,8 @@ def main():
     ap.add_argument("--ktiles", type=int, default=0)
     ap.add_argument("--ntiles", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--permute", type=int, default=0,
+                    help="relabel A with permute_symmetric(seed) first (0 = BASELINE order)")
     ap.add_argument("--no-fuse", action="store_true", help="RunOptions::fuse_k = false")
     ap.add_argument("--no-split", action="store_true", help="RunOptions::split_local = false")
     ap.add_argument("--lookahead", type=int, default=2, help="RunOptions::lookahead")

@@ -232,6 +232,18 @@ int rdmm_gen_finish(rdmm_gen_state* st, int dtype_bytes, uint32_t* row_ptr,
                     uint32_t* col_idx, void* values);
 void rdmm_gen_abort(rdmm_gen_state* st);
 
+/* permute_symmetric (gen.hpp:134-155): P A P^T with the reference's
+ * Fisher-Yates permutation over rng::at(seed, i).  Device CSR in, device CSR
+ * out (out_row_ptr rows+1, out_col_idx / out_values nnz; caller-owned).
+ * RDMM_ERR_DIMENSION if rows != cols.  Synchronous on `stream`. */
+int rdmm_permute_symmetric(uint32_t rows, uint32_t cols, uint64_t nnz,
+                           const uint32_t* row_ptr, const uint32_t* col_idx,
+                           const void* values, int dtype_bytes, uint64_t seed,
+                           uint32_t* out_row_ptr, uint32_t* out_col_idx,
+                           void* out_values, rdmm_stream_t stream);
+/* The permutation alone, on the host: perm[old index] = new index. */
+int rdmm_permutation(uint32_t n, uint64_t seed, uint32_t* perm);
+
 /* ================================================================ fabric */
 /*
  * The one-sided fabric (reference fabric.hpp:26-575) on B200:

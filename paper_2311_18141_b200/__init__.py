@@ -6,8 +6,9 @@ the CUDA library and fails loudly if it has not been built.
 """
 from . import _lib  # noqa: F401  (loads librdmm_cuda.so or raises)
 from ._lib import (CudaError, DimensionError, FabricError, HeapExhaustedError,  # noqa: F401
-                   InvalidArgument, ProtocolError, QueueFullError, RdmmError)
-from .tile import (DeviceCsr, FlopMeter, csr_add, dense_add_into, random_dense,  # noqa: F401
-                   real_twin, rmat, spgemm_local, spgemm_terms, spmm_local, uniform_tiles)
+                   InvalidArgument, MmioError, ProtocolError, QueueFullError, RdmmError)
+from .tile import (DeviceCsr, FlopMeter, csr_add, dense_add_into, permutation,  # noqa: F401
+                   permute_symmetric, random_dense, real_twin, rmat, spgemm_local, spgemm_terms,
+                   spmm_local, uniform_tiles)
 
 __version__ = "0.1.0"

@@ -120,6 +120,9 @@ rdmm_gen_uniform_tiles_begin = _fn("rdmm_gen_uniform_tiles_begin",
                                    [u64, u64, u32, dbl, u64, P(vp), P(u64)])
 rdmm_gen_finish = _fn("rdmm_gen_finish", [vp, cint, vp, vp, vp])
 rdmm_gen_abort = _fn("rdmm_gen_abort", [vp], None)
+rdmm_permute_symmetric = _fn("rdmm_permute_symmetric",
+                             [u32, u32, u64, vp, vp, vp, cint, u64, vp, vp, vp, vp])
+rdmm_permutation = _fn("rdmm_permutation", [u32, u64, vp])
 
 
 # ---- fabric (control plane + heaps), include/rdmm_cuda.h

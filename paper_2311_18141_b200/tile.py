@@ -253,6 +253,27 @@ def uniform_tiles(m: int, k: int, p: int, d: float, seed: int, dtype=torch.float
         return _finish(st, nnz.value, m, k, dtype, device)
 
 
+def permute_symmetric(a: DeviceCsr, seed: int, stream=None) -> DeviceCsr:
+    """P A P^T with the reference's Fisher-Yates permutation (gen.hpp:134-155),
+    relabelled and row-sorted on the device; bit-identical to the reference."""
+    out = DeviceCsr.empty(a.rows, a.cols, a.nnz, dtype=a.dtype, device=a.device)
+    L.check(L.rdmm_permute_symmetric(a.rows, a.cols, a.nnz, a.row_ptr.data_ptr(),
+                                     a.col_idx.data_ptr(), a.values.data_ptr(), _wcode(a.dtype),
+                                     seed, out.row_ptr.data_ptr(), out.col_idx.data_ptr(),
+                                     out.values.data_ptr(), _stream(stream)),
+            "permute_symmetric")
+    return out
+
+
+def permutation(n: int, seed: int):
+    """The permutation alone (host): perm[old] = new (gen.hpp:141-147)."""
+    import numpy as np
+
+    perm = np.empty(n, np.uint32)
+    L.check(L.rdmm_permutation(n, seed, perm.ctypes.data), "permutation")
+    return perm
+
+
 def random_dense(rows: int, cols: int, seed: int, max_value: int = 3, dtype=torch.float32,
                  device="cuda", stream=None) -> torch.Tensor:
     """random_dense (gen.hpp:174-181)."""

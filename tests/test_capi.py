@@ -70,3 +70,22 @@ def test_library_is_sm100a_only():
         pytest.skip("cuobjdump unavailable")
     archs = set(re.findall(r"sm_(\d+a?)", out))
     assert archs == {"100a"}, archs
+
+
+def test_host_permutation_matches_reference(golden, orc):
+    """rdmm_permutation (host part of permute_symmetric, gen.hpp:141-147):
+    relabelling rmat(8, 8, seed=1) with it reproduces the reference golden."""
+    import numpy as np
+
+    from paper_2311_18141_b200.tile import permutation
+
+    a = orc.rmat(8, 8, seed=1)
+    perm = permutation(a.rows, 5).astype(np.int64)
+    assert np.array_equal(np.sort(perm), np.arange(a.rows))
+    r = np.repeat(np.arange(a.rows), np.diff(a.row_ptr.astype(np.int64)))
+    nr, nc = perm[r], perm[a.col_idx.astype(np.int64)]
+    order = np.lexsort((nc, nr))
+    rp = np.concatenate([[0], np.cumsum(np.bincount(nr, minlength=a.rows))])
+    assert np.array_equal(rp, golden["perm8_rp"])
+    assert np.array_equal(nc[order], golden["perm8_ci"])
+    assert np.array_equal(a.values[order], golden["perm8_v"])

@@ -80,3 +80,30 @@ def test_structural_goldens_at_benchmark_scale(rd):
     assert e.nnz == 67_108_864
     assert int(deg.max()) == 39
     assert int((deg == 0).sum()) == 1
+
+
+def test_permute_symmetric_matches_reference(rd, golden, orc):
+    """gen.hpp:134-155 on the device: bit-identical to the reference golden
+    (perm8 = permute_symmetric(rmat(8, 8, seed=1), 5)) and to the oracle at a
+    larger scale, fp32 and fp64."""
+    same(rd.permute_symmetric(rd.rmat(8, 8, seed=1), 5), golden, "perm8")
+    for dt, ndt in ((torch.float32, np.float32), (torch.float64, np.float64)):
+        a = orc.rmat(14, 8, seed=1, dtype=ndt)
+        a.values[:] = np.arange(a.nnz) % 7 - 3  # distinct values follow their entries
+        want = orc.permute_symmetric(a, 11)
+        d = rd.DeviceCsr.from_host(a.rows, a.cols, a.row_ptr, a.col_idx, a.values)
+        assert d.dtype == dt
+        rp, ci, vv = rd.permute_symmetric(d, 11).to_host()
+        assert np.array_equal(rp, want.row_ptr) and np.array_equal(ci, want.col_idx)
+        assert np.array_equal(vv, want.values)
+
+
+def test_permute_symmetric_edges(rd):
+    e = rd.DeviceCsr.from_host(4, 4, np.zeros(5, np.uint32), np.zeros(0, np.uint32),
+                               np.zeros(0, np.float32))
+    rp, ci, vv = rd.permute_symmetric(e, 3).to_host()
+    assert np.array_equal(rp, np.zeros(5)) and len(ci) == 0
+    r = rd.DeviceCsr.from_host(2, 3, np.array([0, 1, 1], np.uint32), np.array([2], np.uint32),
+                               np.array([1.0], np.float32))
+    with pytest.raises(rd.DimensionError):
+        rd.permute_symmetric(r, 1)
