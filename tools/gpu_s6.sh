@@ -8,4 +8,5 @@ for kt in 4 8; do
 done
 timeout 600 $T bench.py --gpus 2 --steps 10 --permute 7 --lookahead 1 --no-cpu-baseline > $O/cfg3_perm_la1.json 2> $O/cfg3_perm_la1.err
 timeout 900 $T bench.py --gpus 2 --steps 3 --config cfg4 --permute 7 --mtiles 16 --no-cpu-baseline > $O/cfg4_perm_m16.json 2> $O/cfg4_perm_m16.err
+timeout 900 $T bench.py --gpus 2 --steps 3 --config cfg4 --permute 7 --variant stationary_c --mtiles 2 --no-cpu-baseline > $O/cfg4_perm_sc.json 2> $O/cfg4_perm_sc.err
 echo finished
