@@ -10,6 +10,7 @@
 #include <string>
 
 #include "rdmm/algos.hpp"
+#include "rdmm/analytics.hpp"
 
 using namespace rdmm;
 
@@ -251,6 +252,14 @@ static void test_algos() {
       for (auto& pr : rep.triples) tr.insert(pr.begin(), pr.end());
       REQUIRE(tr.size() == 27 && rep.total_multiplies() == 27);
       REQUIRE(rep.checksum == matrix_checksum(C));
+      // analytics.hpp:66-90 over the run's own per-k-step flop table
+      ImbalanceReport imb = run_imbalance(rep);
+      std::uint64_t staged = 0;
+      for (auto& r : imb.stage_flops)
+        for (auto x : r) staged += x;
+      REQUIRE(staged == rep.total_flops() && imb.stage_flops.size() == 4);
+      REQUIRE(imb.per_stage_flop_imbalance + 1e-12 >= imb.end_to_end_flop_imbalance);
+      REQUIRE(imb.end_to_end_flop_imbalance >= 1.0);
     }
     // SpGEMM
     {
