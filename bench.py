@@ -33,8 +33,8 @@ CONFIGS = {
     # BASELINE.json configs[0..4]
     "cfg1": dict(kind="spmm", gen="rmat", scale=16, ef=8, n=128,
                  desc="SpMM R-MAT s16 ef8 x dense 65536x128 fp32"),
-    "cfg2": dict(kind="spgemm", gen="rmat", scale=17, ef=8,
-                 desc="SpGEMM A*A, R-MAT s17 ef8"),
+    "cfg2": dict(kind="spgemm", gen="rmat", scale=17, ef=8, variant="stationary_c",
+                 grid="square", desc="SpGEMM A*A, R-MAT s17 ef8"),
     "cfg3": dict(kind="spmm", gen="rmat", scale=22, ef=16, n=128,
                  desc="SpMM R-MAT s22 ef16 x dense 4194304x128 fp32"),
     "cfg4": dict(kind="spgemm", gen="rmat", scale=20, ef=8,
@@ -142,11 +142,17 @@ def layout(cfg, P, args):
     the narrow N/P kernel, whose cost follows the 4M rows it walks, not the
     nonzeros: measured 2x slower at P = 2 (profiles/README.md).
     SpGEMM: a P x 1 grid with 4P row tiles of C and K = P, so the
-    locality-aware work stealing can rebalance R-MAT's row skew.
+    locality-aware work stealing can rebalance R-MAT's row skew (cfg4);
+    cfg2 runs stationary-C on a square-ish pr x pc grid (4 pr row tiles).
     """
     n_rows = 1 << cfg["scale"]
     if args.grid:
         pr, pc = (int(x) for x in args.grid.split("x"))
+    elif cfg.get("grid") == "square":
+        # cfg2 compares the stationary variants on a square-ish 2D grid
+        # (BASELINE configs[1]; 2x2 at 4 GPUs, profiles/r1_s5/)
+        pc = max(d for d in range(1, int(P ** 0.5) + 1) if P % d == 0)
+        pr = P // pc
     else:
         # split columns only while every rank keeps >= 128 fp32 columns
         pc = 1
@@ -682,7 +688,8 @@ def main():
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
     if args.variant is None:
-        args.variant = "stationary_c" if cfg["kind"] == "spmm" else "ws_locality"
+        args.variant = cfg.get("variant") or (
+            "stationary_c" if cfg["kind"] == "spmm" else "ws_locality")
 
     if args.impl == "reference":
         out = run_reference(args)
