@@ -37,8 +37,8 @@ CONFIGS = {
                  grid="square", desc="SpGEMM A*A, R-MAT s17 ef8"),
     "cfg3": dict(kind="spmm", gen="rmat", scale=22, ef=16, n=128,
                  desc="SpMM R-MAT s22 ef16 x dense 4194304x128 fp32"),
-    "cfg4": dict(kind="spgemm", gen="rmat", scale=20, ef=8,
-                 desc="SpGEMM A*A, R-MAT s20 ef8"),
+    "cfg4": dict(kind="spgemm", gen="rmat", scale=20, ef=8, variant="ws_locality",
+                 grid="square", desc="SpGEMM A*A, R-MAT s20 ef8"),
     "cfg5": dict(kind="spmm", gen="er", scale=22, n=256, d=2.0 ** -18,
                  desc="SpMM Erdos-Renyi 2^22, 16 nnz/row x dense N=256 fp32"),
 }
@@ -141,16 +141,15 @@ def layout(cfg, P, args):
     A 1 x P grid (column split) replicates A instead but drops every rank to
     the narrow N/P kernel, whose cost follows the 4M rows it walks, not the
     nonzeros: measured 2x slower at P = 2 (profiles/README.md).
-    SpGEMM: a P x 1 grid with 4P row tiles of C and K = P, so the
-    locality-aware work stealing can rebalance R-MAT's row skew (cfg4);
-    cfg2 runs stationary-C on a square-ish pr x pc grid (4 pr row tiles).
+    SpGEMM: a square-ish pr x pc grid with 4 pr row tiles of C and K = pr
+    (cfg2 stationary-C, cfg4 ws_locality): at 4 GPUs 2x2 beats 4x1 by 1.25x
+    (cfg2) and 1.44x (cfg4), profiles/r1_s5, r1_s9.
     """
     n_rows = 1 << cfg["scale"]
     if args.grid:
         pr, pc = (int(x) for x in args.grid.split("x"))
     elif cfg.get("grid") == "square":
-        # cfg2 compares the stationary variants on a square-ish 2D grid
-        # (BASELINE configs[1]; 2x2 at 4 GPUs, profiles/r1_s5/)
+        # SpGEMM on a square-ish 2D grid (2x2 at 4 GPUs, 4x2 at 8)
         pc = max(d for d in range(1, int(P ** 0.5) + 1) if P % d == 0)
         pr = P // pc
     else:
@@ -277,7 +276,9 @@ def run_ours(args, cfg, dev, rank, world):
         Cm.init()
         reset = Cm.init
     variant = args.variant
-    opts = dict(variant=variant, ws_base="stationary_c", checksum=False, record_events=False,
+    # ws_random steals stationary-A reservations only (algos.hpp:476-533)
+    ws_base = "stationary_a" if variant == "ws_random" else "stationary_c"
+    opts = dict(variant=variant, ws_base=ws_base, checksum=False, record_events=False,
                 fuse_k=not args.no_fuse, lookahead=args.lookahead,
                 split_local=not args.no_split)
     stream = torch.cuda.ExternalStream(f.stream(rank), device=dev)

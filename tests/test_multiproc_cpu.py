@@ -106,7 +106,7 @@ def test_bench_session_and_layout():
     (pr, pc), tiles = bench.layout(bench.CONFIGS["cfg3"], 1, A)
     assert (pr, pc) == (1, 1) and tuple(tiles) == (4194304, 4194304, 128)
     (pr, pc), tiles = bench.layout(bench.CONFIGS["cfg4"], 4, A)
-    assert (pr, pc) == (4, 1) and tiles[0] == (1 << 20) // 16
+    assert (pr, pc) == (2, 2) and tuple(tiles) == ((1 << 20) // 8, (1 << 20) // 2, (1 << 20) // 2)
     # cfg2: stationary variants on a square-ish grid (2x2 at 4, 4x2 at 8, 2x1 at 2)
     for P, grid in ((1, (1, 1)), (2, (2, 1)), (4, (2, 2)), (8, (4, 2))):
         (pr, pc), tiles = bench.layout(bench.CONFIGS["cfg2"], P, A)
