@@ -404,9 +404,12 @@ class DistSparse {  // distmat.hpp:210-398
       for (auto g : {e.row_ptr, e.col_idx, e.values})
         rdmm_record_self_get(ctx.h(), ctx.rank(), g.length);
     } else {
+      // Each buffer is allocated on the stream that fills it: the stream-
+      // ordered pool may hand out a block freed on the compute stream and
+      // orders only the allocating stream behind that free.
       t.row_ptr = DevBuffer(ctx.h(), ctx.rank(), e.row_ptr.length, ctx.stream(1));
-      t.col_idx = DevBuffer(ctx.h(), ctx.rank(), e.col_idx.length, ctx.stream(1));
-      t.values = DevBuffer(ctx.h(), ctx.rank(), e.values.length, ctx.stream(1));
+      t.col_idx = DevBuffer(ctx.h(), ctx.rank(), e.col_idx.length, ctx.stream(2));
+      t.values = DevBuffer(ctx.h(), ctx.rank(), e.values.length, ctx.stream(2));
       hs.push_back(ctx.get_nb(GlobalPtr::of(e.row_ptr), t.row_ptr.get(), 1));
       hs.push_back(ctx.get_nb(GlobalPtr::of(e.col_idx), t.col_idx.get(), 2));
       hs.push_back(ctx.get_nb(GlobalPtr::of(e.values), t.values.get(), 2));

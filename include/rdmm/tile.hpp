@@ -300,7 +300,7 @@ FlopMeter spmm_fused(rdmm_fabric* f, std::uint32_t rank, const std::vector<DevCs
   std::vector<const void*> vv(K), bs(K);
   for (std::size_t k = 0; k < K; ++k) {
     if (a[k].rows != c.rows || a[k].cols != b[k].rows || b[k].cols != c.cols ||
-        b[k].ld != b[0].ld || (k + 1 < K && b[k].rows != col_stride))
+        b[k].ld != b[0].ld || b[k].rows > col_stride)
       throw dimension_error("spmm_fused: dimension mismatch");
     nnz += a[k].nnz;
     tn[k] = a[k].nnz;

@@ -92,11 +92,8 @@ int rdmm_spmm_csr_f64(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
  *   RDMM_SPMM_C_ZERO      C is all-zero on entry (a fresh tile): rows with
  *                         nonzeros are written, C is never read; results are
  *                         identical to the accumulate form on a zero C.
- *   RDMM_SPMM_NO_PREFETCH accepted for compatibility; no effect (the L2
- *                         prefetch it disabled measured slower and was removed).
  */
 #define RDMM_SPMM_C_ZERO 1u
-#define RDMM_SPMM_NO_PREFETCH 2u
 int rdmm_spmm_csr_ex(int dtype_bytes, uint32_t rows, uint32_t cols, uint32_t n,
                      uint64_t nnz, const uint32_t* row_ptr,
                      const uint32_t* col_idx, const void* val, const void* B,
@@ -407,6 +404,10 @@ int rdmm_memcpy(void* dst, const void* src, uint64_t bytes,
                 rdmm_stream_t stream); /* any direction; NULL stream = sync */
 int rdmm_memset(void* dst, int value, uint64_t bytes, rdmm_stream_t stream);
 int rdmm_event_record(rdmm_stream_t stream, void** event);
+/* Timing-enabled event (per-stage device time, RunOptions::time_stages) and
+ * the elapsed milliseconds between two of them (blocks until b completed). */
+int rdmm_timing_event_record(rdmm_stream_t stream, void** event);
+int rdmm_event_elapsed_ms(void* a, void* b, float* ms);
 int rdmm_event_query(void* event, int* done); /* done=1 when complete */
 int rdmm_event_wait(void* event, rdmm_stream_t consumer);
 int rdmm_event_sync(void* event);

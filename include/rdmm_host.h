@@ -84,6 +84,7 @@ typedef struct {
   int checksum;
   int fuse_k;
   int split_local; /* fused stationary-C: local products first on the first tile */
+  int time_stages; /* per-k-step device time of each rank's multiplies (stage_ms) */
 } rdmm_h_options;
 
 #define RDMM_H_MAX_RANKS 64
@@ -110,6 +111,9 @@ typedef struct {
    * rdmm_h_free); ranks hosted by other processes are zero rows. */
   uint32_t nstages;
   uint64_t* stage_flops;
+  /* Per-rank device milliseconds per k tile step (RankStats::stage_ms; with
+   * time_stages), same shape and ownership as stage_flops; NULL otherwise. */
+  double* stage_ms;
 } rdmm_h_report;
 
 int rdmm_h_run_multiply(rdmm_h_fabric* f, rdmm_h_matrix* A, rdmm_h_matrix* B,

@@ -96,7 +96,6 @@ rdmm_spmm_csr_f64 = _fn("rdmm_spmm_csr_f64", _spmm_args)
 rdmm_spmm_csr_ex = _fn("rdmm_spmm_csr_ex", [cint, u32, u32, u32, u64, vp, vp, vp, vp, u64, vp,
                                             u64, C.c_uint, vp, sz, vp, P(u64)])
 SPMM_C_ZERO = 1
-SPMM_NO_PREFETCH = 2
 
 
 class SpgemmTerm(C.Structure):

@@ -167,6 +167,7 @@ struct Local {
   bool sink = false;
   std::vector<rdmm_event> events;
   unsigned long long* atomic_slot = nullptr;  // pinned, device-space fetch_add
+  cudaStream_t atomic_stream = nullptr;       // idle stream for device fetch_add
 };
 
 using TKey = std::tuple<uint32_t, uint32_t, int64_t>;
@@ -336,7 +337,16 @@ extern "C" int rdmm_fabric_create(const rdmm_fabric_config* cfg,
     return fail(RDMM_ERR_FABRIC, "nranks exceeds 64");
   if (cfg->nlocal == 0 || cfg->first_local + cfg->nlocal > cfg->nranks)
     return fail(RDMM_ERR_FABRIC, "bad local rank range");
-  auto f = std::make_unique<rdmm_fabric>();
+  // Every error return below runs the deleter: the abort flag releases peers
+  // waiting in wait_all_published / barrier_n, and destroy unlinks the shm
+  // name and frees the heaps, streams and IPC mappings created so far.
+  struct Cleanup {
+    void operator()(rdmm_fabric* p) const {
+      rdmm_fabric_abort(p, "fabric creation failed");
+      rdmm_fabric_destroy(p);
+    }
+  };
+  std::unique_ptr<rdmm_fabric, Cleanup> f(new rdmm_fabric());
   f->cfg = *cfg;
   f->cfg.devices = nullptr;
   f->cfg.session = nullptr;
@@ -440,6 +450,7 @@ extern "C" int rdmm_fabric_create(const rdmm_fabric_config* cfg,
       RDMM_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     RDMM_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&L->atomic_slot), 64,
                                 cudaHostAllocPortable));
+    RDMM_CUDA_TRY(cudaStreamCreateWithFlags(&L->atomic_stream, cudaStreamNonBlocking));
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, L->device) == cudaSuccess) {
       uint64_t thr = ~0ull;
@@ -518,6 +529,7 @@ extern "C" void rdmm_fabric_destroy(rdmm_fabric* f) {
         cudaStreamSynchronize(s);
         cudaStreamDestroy(s);
       }
+    if (L->atomic_stream) cudaStreamDestroy(L->atomic_stream);
     if (L->heap.base) cudaFree(L->heap.base);
     if (L->atomic_slot) cudaFreeHost(L->atomic_slot);
   }
@@ -737,11 +749,12 @@ extern "C" int rdmm_fetch_add_i64(rdmm_fabric* f, uint32_t caller,
     *old = __atomic_fetch_add(p, delta, __ATOMIC_SEQ_CST);
   } else {
     // device-heap cell: one system-scope atomic over NVLink from the
-    // caller's GPU (slow path; reservations use control cells)
+    // caller's GPU (slow path; reservations use control cells), on an idle
+    // stream so it does not wait for the queued compute
     RDMM_CUDA_TRY(cudaSetDevice(C->device));
     auto* p = reinterpret_cast<unsigned long long*>(dev_addr(f, C, cell));
-    k_fetch_add<<<1, 1, 0, C->streams[0]>>>(p, delta, C->atomic_slot);
-    RDMM_CUDA_TRY(cudaStreamSynchronize(C->streams[0]));
+    k_fetch_add<<<1, 1, 0, C->atomic_stream>>>(p, delta, C->atomic_slot);
+    RDMM_CUDA_TRY(cudaStreamSynchronize(C->atomic_stream));
     *old = static_cast<int64_t>(*C->atomic_slot);
   }
   f->record_atomic(caller, cell.rank);
@@ -984,6 +997,18 @@ extern "C" int rdmm_event_record(rdmm_stream_t stream, void** event) {
   RDMM_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   RDMM_CUDA_TRY(cudaEventRecord(e, as_stream(stream)));
   *event = e;
+  return RDMM_OK;
+}
+extern "C" int rdmm_timing_event_record(rdmm_stream_t stream, void** event) {
+  cudaEvent_t e;
+  RDMM_CUDA_TRY(cudaEventCreate(&e));
+  RDMM_CUDA_TRY(cudaEventRecord(e, as_stream(stream)));
+  *event = e;
+  return RDMM_OK;
+}
+extern "C" int rdmm_event_elapsed_ms(void* a, void* b, float* ms) {
+  RDMM_CUDA_TRY(cudaEventSynchronize(static_cast<cudaEvent_t>(b)));
+  RDMM_CUDA_TRY(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(a), static_cast<cudaEvent_t>(b)));
   return RDMM_OK;
 }
 extern "C" int rdmm_event_query(void* event, int* done) {

@@ -100,6 +100,7 @@ RunOptions opts_of(const rdmm_h_options* o) {
   r.checksum = o->checksum != 0;
   r.fuse_k = o->fuse_k != 0;
   r.split_local = o->split_local != 0;
+  r.time_stages = o->time_stages != 0;
   return r;
 }
 
@@ -128,7 +129,11 @@ void fill(const RunReport& r, rdmm_h_report* out) {
     out->total_seconds[p] = s.total_seconds;
   }
   std::size_t ns = 0;
-  for (auto& s : r.per_rank) ns = std::max(ns, s.stage_flops.size());
+  bool timed = false;
+  for (auto& s : r.per_rank) {
+    ns = std::max(ns, std::max(s.stage_flops.size(), s.stage_ms.size()));
+    timed |= !s.stage_ms.empty();
+  }
   out->nstages = uint32_t(ns);
   if (ns && !r.per_rank.empty()) {
     out->stage_flops =
@@ -136,6 +141,12 @@ void fill(const RunReport& r, rdmm_h_report* out) {
     for (std::size_t p = 0; p < r.per_rank.size(); ++p)
       std::copy(r.per_rank[p].stage_flops.begin(), r.per_rank[p].stage_flops.end(),
                 out->stage_flops + p * ns);
+    if (timed) {
+      out->stage_ms = static_cast<double*>(std::calloc(r.per_rank.size() * ns, sizeof(double)));
+      for (std::size_t p = 0; p < r.per_rank.size(); ++p)
+        std::copy(r.per_rank[p].stage_ms.begin(), r.per_rank[p].stage_ms.end(),
+                  out->stage_ms + p * ns);
+    }
   }
   out->ntriples = nt;
   if (nt) {

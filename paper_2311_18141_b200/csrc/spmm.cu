@@ -37,6 +37,21 @@ template <>
 struct VecOf<double, 2> {
   using type = double2;
 };
+// 32-byte vectors: one 256-bit load per lane (LDG.E.ENL2.256 on sm_100a).
+struct __align__(32) float8 {
+  float4 lo, hi;
+};
+struct __align__(32) double4x {
+  double2 lo, hi;
+};
+template <>
+struct VecOf<float, 8> {
+  using type = float8;
+};
+template <>
+struct VecOf<double, 4> {
+  using type = double4x;
+};
 template <>
 struct VecOf<float, 1> {
   using type = float;
@@ -53,6 +68,12 @@ __device__ __forceinline__ float4 vfma(float a, float4 b, float4 c) {
 __device__ __forceinline__ double2 vfma(double a, double2 b, double2 c) {
   return make_double2(fma(a, b.x, c.x), fma(a, b.y, c.y));
 }
+__device__ __forceinline__ float8 vfma(float a, float8 b, float8 c) {
+  return float8{vfma(a, b.lo, c.lo), vfma(a, b.hi, c.hi)};
+}
+__device__ __forceinline__ double4x vfma(double a, double4x b, double4x c) {
+  return double4x{vfma(a, b.lo, c.lo), vfma(a, b.hi, c.hi)};
+}
 __device__ __forceinline__ float vfma(float a, float b, float c) {
   return fmaf(a, b, c);
 }
@@ -65,6 +86,12 @@ __device__ __forceinline__ float4 vadd(float4 a, float4 b) {
 __device__ __forceinline__ double2 vadd(double2 a, double2 b) {
   return make_double2(a.x + b.x, a.y + b.y);
 }
+__device__ __forceinline__ float8 vadd(float8 a, float8 b) {
+  return float8{vadd(a.lo, b.lo), vadd(a.hi, b.hi)};
+}
+__device__ __forceinline__ double4x vadd(double4x a, double4x b) {
+  return double4x{vadd(a.lo, b.lo), vadd(a.hi, b.hi)};
+}
 __device__ __forceinline__ float vadd(float a, float b) { return a + b; }
 __device__ __forceinline__ double vadd(double a, double b) { return a + b; }
 __device__ __forceinline__ uint64_t umin(uint64_t a, uint64_t b) {
@@ -73,6 +100,59 @@ __device__ __forceinline__ uint64_t umin(uint64_t a, uint64_t b) {
 __device__ __forceinline__ uint64_t umax(uint64_t a, uint64_t b) {
   return a > b ? a : b;
 }
+// Read-only gather / streaming load / streaming store of one vector.
+template <typename V>
+__device__ __forceinline__ V ldg_v(const V* p) {
+  return __ldg(p);
+}
+template <>
+__device__ __forceinline__ float8 ldg_v(const float8* p) {
+  float8 r;
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(r.lo.x), "=f"(r.lo.y), "=f"(r.lo.z), "=f"(r.lo.w), "=f"(r.hi.x),
+                 "=f"(r.hi.y), "=f"(r.hi.z), "=f"(r.hi.w)
+               : "l"(p));
+  return r;
+}
+template <>
+__device__ __forceinline__ double4x ldg_v(const double4x* p) {
+  double4x r;
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(r.lo.x), "=d"(r.lo.y), "=d"(r.hi.x), "=d"(r.hi.y)
+               : "l"(p));
+  return r;
+}
+template <typename V>
+__device__ __forceinline__ V ldcs_v(const V* p) {
+  return __ldcs(p);
+}
+template <>
+__device__ __forceinline__ float8 ldcs_v(const float8* p) {
+  const float4* q = reinterpret_cast<const float4*>(p);
+  return float8{__ldcs(q), __ldcs(q + 1)};
+}
+template <>
+__device__ __forceinline__ double4x ldcs_v(const double4x* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  return double4x{__ldcs(q), __ldcs(q + 1)};
+}
+template <typename V>
+__device__ __forceinline__ void stcs_v(V* p, V v) {
+  __stcs(p, v);
+}
+template <>
+__device__ __forceinline__ void stcs_v(float8* p, float8 v) {
+  float4* q = reinterpret_cast<float4*>(p);
+  __stcs(q, v.lo);
+  __stcs(q + 1, v.hi);
+}
+template <>
+__device__ __forceinline__ void stcs_v(double4x* p, double4x v) {
+  double2* q = reinterpret_cast<double2*>(p);
+  __stcs(q, v.lo);
+  __stcs(q + 1, v.hi);
+}
+
 template <typename V>
 __device__ __forceinline__ V vzero() {
   V v;
@@ -90,10 +170,10 @@ struct SpmmArgs {
   T* __restrict__ head_val;  // [nchunks][wstride]
   T* __restrict__ tail_val;  // [nchunks][wstride]
   int32_t* __restrict__ tail_row;  // [nchunks]
+  const uint32_t* __restrict__ chunk_row;  // [nchunks] row holding nonzero c*Q
   uint64_t ldb, ldc;
   uint64_t nnz, Q;
   uint32_t rows, nvec, nchunks, wstride;
-  int prefetch;  // unused (the L2 prefetch of the next window measured slower)
   // Segmented B (fused K-tile products): B row g lives in segment
   // g / seg_rows at row g % seg_rows; nseg == 0 means one contiguous B.
   const T* bseg[16];
@@ -125,6 +205,17 @@ __device__ __forceinline__ const V* brow_ptr(const SpmmArgs<T>& p, const SegTabl
   const uint32_t sg = p.seg_shift < 32 ? (k >> p.seg_shift) : (k / p.seg_rows);
   const uint32_t r = k - sg * p.seg_rows;
   return reinterpret_cast<const V*>(st.base[sg]) + uint64_t(r) * ldbv + voff;
+}
+
+// arr[idx] for a runtime idx without dynamic register indexing (which would
+// put the array in local memory): unrolled predicated selects.
+template <int SL, typename X>
+__device__ __forceinline__ X sel(const X (&arr)[SL], uint32_t idx) {
+  X v = arr[0];
+#pragma unroll
+  for (int j = 1; j < SL; ++j)
+    if (idx == uint32_t(j)) v = arr[j];
+  return v;
 }
 
 template <int G>
@@ -205,15 +296,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
   for (uint32_t c = worker; c < p.nchunks; c += nworkers) {
     const uint64_t lo = uint64_t(c) * p.Q;
     const uint64_t hi = umin(lo + p.Q, p.nnz);
-    // row containing nonzero `lo`: largest r with rp[r] <= lo
-    uint32_t l = 0, h = p.rows;
-    while (h - l > 1) {
-      const uint32_t m = (l + h) >> 1;
-      if (__ldg(p.rp + m) <= lo)
-        l = m;
-      else
-        h = m;
-    }
+    // row containing nonzero `lo` (spmm_chunk_rows)
+    const uint32_t l = __ldg(p.chunk_row + c);
     uint32_t rb = l, row = l;
     uint32_t rew[SL];
     win_load<G, SL>(rew, p.rp, rb, p.rows, lane);
@@ -257,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll
           for (int u = 0; u < kU; ++u) {
             const int q = t + u;
-            const uint32_t k = __shfl_sync(gm, kk[q / G], q % G, G);
+            const uint32_t k = __shfl_sync(gm, sel<SL>(kk, q / G), q % G, G);
             if (q < int(cnt)) {
               const V* brow = brow_ptr<T, V, SEG>(p, segs, Bv, k, ldbv, lane);
 #pragma unroll
@@ -268,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll
           for (int u = 0; u < kU; ++u) {
             const int q = t + u;
-            const T a = __shfl_sync(gm, aa[q / G], q % G, G);
+            const T a = __shfl_sync(gm, sel<SL>(aa, q / G), q % G, G);
             if (q < int(cnt)) {
               const uint64_t pos = w + q;
               if (pos >= rend) {
@@ -336,6 +420,585 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
+
+// Chunk start rows: chunk c begins at nonzero c*Q, inside the row r with
+// rp[r] <= c*Q < rp[r+1].  One coalesced pass over the row pointer replaces
+// a 22-step dependent binary search per chunk in the SpMM kernels.
+__global__ void spmm_chunk_rows(const uint32_t* __restrict__ rp, uint32_t rows, uint64_t Q,
+                                uint32_t nchunks, uint32_t* __restrict__ chunk_row) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += gridDim.x * blockDim.x) {
+    const uint64_t s = __ldg(rp + r), e = __ldg(rp + r + 1);
+    for (uint64_t c = (s + Q - 1) / Q; c * Q < e && c < nchunks; ++c)
+      chunk_row[c] = r;
+  }
+}
+
+// cp.async (LDGSTS) helpers: 4/8-byte global -> shared copies that do not
+// occupy registers while in flight; src_size 0 zero-fills.
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, bool ok, int bytes) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const int n = ok ? bytes : 0;
+  if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(n));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool ok) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const int n = ok ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Narrow rows (N < 128 fp32: a B row is L vectors of VEC elements, L < 32):
+// the warp is ONE worker streaming its nnz chunks, split into S = 32/L slots
+// of L lanes; a step feeds S consecutive nonzeros to the S slots (one B-row
+// gather per slot, U steps = U gathers per lane in flight), so every row
+// boundary is warp-uniform: no divergent per-group row flushes, and a step
+// inside a row is U-independent FMAs with one compare.  The chunk's col/val
+// stream is staged in a per-warp shared-memory ring NST windows ahead with
+// cp.async (continuing across the warp's chunks), so the A stream's latency
+// never stalls the gathers; the next chunk's start row is prefetched too.
+// A row is accumulated as S slot partials and combined by a reduce-scatter
+// over the slots when the stream crosses the row's end (each level halves
+// the vector a lane keeps: log2(S) shuffles of VEC/2, VEC/4, ... elements);
+// lane (slot, v) then owns elements [v*VEC + coff, +LEN) of the row and
+// stores them.  Rows cut by chunk boundaries leave head/tail partials for
+// spmm_fixup as in spmm_stream.  Summation order: fixed slot partials and
+// tree, then C -- deterministic, exact for integer data, within the fp
+// tolerance otherwise.
+template <typename T, int VEC, int S, bool CZERO, int MINB, bool SEG>
+__global__ void __launch_bounds__(kThreads, MINB)
+    spmm_slots(const SpmmArgs<T> p) {
+  using V = typename VecOf<T, VEC>::type;
+  constexpr int L = 32 / S;                // lanes (vectors) per slot
+  // steps per batch = gathers in flight per lane: 128 bytes of B per lane,
+  // and at most 64 nonzeros per staged window
+  constexpr int UB = sizeof(V) >= 32 ? 4 : 8;
+  constexpr int U = UB * S > 64 ? 64 / S : UB;
+  constexpr int STEP = S * U;              // nonzeros per batch
+  constexpr int W = STEP > 32 ? STEP : 32; // nonzeros per staged window (<= 64)
+  constexpr int SLW = W / 32;              // staged col/val per lane
+  constexpr int NST = 4;                   // ring stages (windows in flight)
+  constexpr int WARPS = kThreads / 32;
+  constexpr int LOGS = S == 1 ? 0 : S == 2 ? 1 : S == 4 ? 2 : S == 8 ? 3 : S == 16 ? 4 : 5;
+  constexpr int LOGV = VEC == 1 ? 0 : VEC == 2 ? 1 : VEC == 4 ? 2 : 3;
+  constexpr int SCAT = LOGS < LOGV ? LOGS : LOGV;  // scatter levels
+  constexpr int LEN = VEC >> SCAT;                 // elements a lane owns at the end
+  __shared__ SegTable<T> segs;
+  __shared__ uint32_t s_ci[WARPS][NST][W];
+  __shared__ T s_val[WARPS][NST][W];
+  load_segs<T, SEG>(p, segs);
+  const uint32_t lane = threadIdx.x & 31u, slot = lane / L, v = lane % L;
+  const uint32_t wib = threadIdx.x >> 5;
+  const uint32_t warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = gridDim.x * WARPS;
+  const V* __restrict__ Bv = reinterpret_cast<const V*>(p.B);
+  T* __restrict__ Cs = p.C;
+  const uint64_t ldbv = p.ldb / VEC;
+  const bool colok = v < p.nvec;
+  // element offset of this lane's share after the reduce-scatter, and
+  // whether it stores (slots beyond the scatter levels hold copies)
+  uint32_t coff = 0;
+#pragma unroll
+  for (int lv = 0; lv < SCAT; ++lv)
+    if (slot & (1u << lv)) coff += VEC >> (lv + 1);
+  const bool owner = colok && (slot >> SCAT) == 0;
+  const uint32_t col0 = v * VEC + coff;  // first owned column within the row
+  constexpr unsigned full = 0xffffffffu;
+  // positions fit in 32 bits: row_ptr is uint32 (tile.hpp:17)
+  const uint32_t nnz = uint32_t(p.nnz), Q = uint32_t(p.Q);
+  auto chunk_hi = [&](uint32_t c) { return uint32_t(umin(uint64_t(c) * Q + Q, nnz)); };
+
+  // issue side of the ring: windows of the warp's chunks in consume order
+  uint32_t ic = warp, iw = warp * Q, ist = 0;
+  auto issue = [&]() {
+    if (ic < p.nchunks) {
+      const uint32_t h = chunk_hi(ic);
+#pragma unroll
+      for (int j = 0; j < SLW; ++j) {
+        const uint32_t idx = iw + lane + 32 * j;
+        const bool ok = idx < h;
+        cp_async(&s_ci[wib][ist][lane + 32 * j], p.ci + (ok ? idx : 0), ok, 4);
+        cp_async(&s_val[wib][ist][lane + 32 * j], p.val + (ok ? idx : 0), ok, int(sizeof(T)));
+      }
+      iw += W;
+      if (iw >= h) {
+        ic += nwarps;
+        iw = ic * Q;
+      }
+    }
+    cp_async_commit();
+    ist = ist + 1 == NST ? 0 : ist + 1;
+  };
+#pragma unroll
+  for (int q = 0; q < NST - 1; ++q) issue();
+
+  // reduce-scatter the S slot partials into out[0..LEN)
+  auto reduce = [&](const V& acc, T (&out)[LEN]) {
+    T r[VEC];
+    const T* pa = reinterpret_cast<const T*>(&acc);
+#pragma unroll
+    for (int x = 0; x < VEC; ++x) r[x] = pa[x];
+#pragma unroll
+    for (int lv = 0; lv < LOGS; ++lv) {
+      const int off = L << lv;
+      if (lv < SCAT) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int half = VEC >> (lv + 1);
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int x = 0; x < VEC / 2; ++x) {
+          if (x < half) {
+            const T send = upper ? r[x] : r[x + half];
+            const T keep = upper ? r[x + half] : r[x];
+            r[x] = keep + __shfl_xor_sync(full, send, off);
+          }
+        }
+      } else {
+        r[0] += __shfl_xor_sync(full, r[0], off);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < LEN; ++x) out[x] = r[x];
+  };
+  // C's initial elements of this lane's share, loaded when the row starts
+  // and added after the tree (the load's latency hides behind the gathers)
+  auto cload = [&](uint32_t row, bool starts, T (&cin)[LEN]) {
+#pragma unroll
+    for (int x = 0; x < LEN; ++x)
+      cin[x] = (!CZERO && starts && owner) ? __ldcs(Cs + uint64_t(row) * p.ldc + col0 + x) : T(0);
+  };
+  auto put = [&](T* dst, const T (&o)[LEN]) {
+#pragma unroll
+    for (int x = 0; x < LEN; ++x) dst[x] = o[x];
+  };
+  auto put_cs = [&](T* dst, const T (&o)[LEN]) {
+#pragma unroll
+    for (int x = 0; x < LEN; ++x) __stcs(dst + x, o[x]);
+  };
+
+  uint32_t cst = 0;  // consume-side ring stage
+  uint32_t nrow = warp < p.nchunks ? __ldg(p.chunk_row + warp) : 0;
+  for (uint32_t c = warp; c < p.nchunks; c += nwarps) {
+    const uint32_t lo = c * Q, hi = chunk_hi(c);
+    uint32_t row = nrow, rb = row;
+    uint32_t rew[1];
+    win_load<32, 1>(rew, p.rp, rb, p.rows, lane);
+    bool starts = __ldg(p.rp + row) >= lo;
+    if (c + nwarps < p.nchunks) nrow = __ldg(p.chunk_row + c + nwarps);
+    uint32_t rend = win_get<32, 1>(rew, 0, full);
+    uint32_t rstart = lo;
+    V acc = vzero<V>();
+    T cin[LEN];
+    cload(row, starts, cin);
+    // flush the current row (it ends at rend) and move to the next one
+    auto flush = [&]() {
+      T o[LEN];
+      reduce(acc, o);
+      if (owner) {
+        if (starts) {
+          if (!CZERO)
+#pragma unroll
+            for (int x = 0; x < LEN; ++x) o[x] = cin[x] + o[x];
+          put_cs(Cs + uint64_t(row) * p.ldc + col0, o);
+        } else {
+          put(p.head_val + uint64_t(c) * p.wstride + col0, o);
+        }
+      }
+      rstart = rend;
+      for (;;) {  // next row holding position rstart (skips empty rows)
+        const uint32_t d = rows_done<32, 1>(rew, rstart, full);
+        if (d < 32u) {
+          row = rb + d;
+          rend = win_get<32, 1>(rew, d, full);
+          break;
+        }
+        rb += 32;
+        win_load<32, 1>(rew, p.rp, rb, p.rows, lane);
+      }
+      starts = true;
+      acc = vzero<V>();
+      cload(row, true, cin);
+    };
+    for (uint32_t w = lo; w < hi; w += W) {
+      issue();
+      cp_async_wait<NST - 1>();
+      __syncwarp();
+      const uint32_t* kw = s_ci[wib][cst];
+      const T* aw = s_val[wib][cst];
+#pragma unroll 1
+      for (int t = 0; t < W; t += STEP) {
+        const uint32_t b0 = w + uint32_t(t);
+        if (b0 >= hi) break;
+        V bv[U];
+        T av[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t q = uint32_t(t + u * S) + slot;
+          const uint32_t k = kw[q];  // zero-filled past the chunk: a harmless row-0 load
+          av[u] = aw[q];
+          if (colok) bv[u] = ldg_v(brow_ptr<T, V, SEG>(p, segs, Bv, k, ldbv, v));
+        }
+        if (b0 + STEP <= hi) {
+          // whole batch inside the chunk
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t base = b0 + uint32_t(u * S);
+            if (rend >= base + S) {  // the step lies inside the current row
+              acc = vfma(av[u], bv[u], acc);
+            } else {
+              const uint32_t pos = base + slot;
+              do {
+                if (pos >= rstart && pos < rend) acc = vfma(av[u], bv[u], acc);
+                flush();
+              } while (rend < base + S);
+              if (pos >= rstart) acc = vfma(av[u], bv[u], acc);
+            }
+          }
+        } else {
+          // the chunk's last, partial batch
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t base = b0 + uint32_t(u * S);
+            if (base >= hi) break;
+            const uint32_t pos = base + slot;
+            const bool valid = pos < hi;
+            const uint32_t lim = min(base + S, hi);
+            while (rend < lim) {
+              if (valid && pos >= rstart && pos < rend) acc = vfma(av[u], bv[u], acc);
+              flush();
+            }
+            if (valid && pos >= rstart) acc = vfma(av[u], bv[u], acc);
+          }
+        }
+      }
+      __syncwarp();
+      cst = cst + 1 == NST ? 0 : cst + 1;
+    }
+    // the chunk's last row
+    T o[LEN];
+    reduce(acc, o);
+    if (!CZERO && starts)
+#pragma unroll
+      for (int x = 0; x < LEN; ++x) o[x] = cin[x] + o[x];
+    int32_t trow = -1;
+    if (rend <= hi && starts) {
+      if (owner) put_cs(Cs + uint64_t(row) * p.ldc + col0, o);
+    } else {
+      if (owner) put((starts ? p.tail_val : p.head_val) + uint64_t(c) * p.wstride + col0, o);
+      if (starts) trow = int32_t(row);
+    }
+    if (lane == 0) p.tail_row[c] = trow;
+  }
+  cp_async_wait<0>();
+}
+
+// Load N consecutive 4- or 8-byte elements from shared memory (16-byte
+// aligned when N * sizeof(E) >= 16) with the widest loads.
+template <int N, typename E>
+__device__ __forceinline__ void lds_vec(E (&out)[N], const E* src) {
+  constexpr int BYTES = N * int(sizeof(E));
+  if constexpr (BYTES >= 16 && BYTES % 16 == 0) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+    for (int i = 0; i < BYTES / 16; ++i) reinterpret_cast<uint4*>(out)[i] = s4[i];
+  } else if constexpr (BYTES == 8) {
+    *reinterpret_cast<uint2*>(out) = *reinterpret_cast<const uint2*>(src);
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[i] = src[i];
+  }
+}
+
+// Narrow rows with the B-row gathers themselves staged by cp.async (16-byte
+// LDGSTS per lane) into a per-warp shared-memory ring GST batches deep: the
+// gathers in flight no longer live in registers, so each warp keeps GST
+// batches of 32 B rows in flight instead of one (the register-staged
+// spmm_slots stalled on its first FMA of every batch: ncu long_scoreboard,
+// profiles/).  Same slot / row / reduce-scatter logic as spmm_slots; a batch
+// is 32 nonzeros = U steps of S.  Pipeline per warp, one commit group per
+// batch i: {col/val window i+D, gathers of batch i+GST-1}; the gathers of a
+// batch read its col indices from the window ring, D = 2*GST-1 batches
+// ahead, so wait_group(GST-1) covers both.
+template <typename T>
+struct AsyncCfg {
+  static constexpr int VEC = 16 / sizeof(T);
+  static constexpr int GST = 3;            // gather stages in flight
+  static constexpr int D = 2 * GST - 1;    // col/val windows ahead of consumption
+  static constexpr int NA = D + 1;         // col/val ring slots
+  static constexpr int WARPS = kThreads / 32;
+  static size_t smem(int L) {
+    return size_t(WARPS) * (size_t(NA) * 32 * (4 + sizeof(T)) + size_t(GST) * 32 * L * 16);
+  }
+};
+
+template <typename T, int S, bool CZERO, bool SEG>
+__global__ void __launch_bounds__(kThreads, 2)
+    spmm_slots_async(const SpmmArgs<T> p) {
+  using C_ = AsyncCfg<T>;
+  constexpr int VEC = C_::VEC;
+  using V = typename VecOf<T, VEC>::type;
+  constexpr int L = 32 / S;   // lanes (16-byte vectors) per slot
+  constexpr int U = 32 / S;   // steps per batch of 32 nonzeros
+  constexpr int GST = C_::GST, D = C_::D, NA = C_::NA, WARPS = C_::WARPS;
+  constexpr int LOGS = S == 1 ? 0 : S == 2 ? 1 : S == 4 ? 2 : S == 8 ? 3 : S == 16 ? 4 : 5;
+  constexpr int LOGV = VEC == 2 ? 1 : 2;
+  constexpr int SCAT = LOGS < LOGV ? LOGS : LOGV;
+  constexpr int LEN = VEC >> SCAT;
+  __shared__ SegTable<T> segs;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  load_segs<T, SEG>(p, segs);
+  const uint32_t lane = threadIdx.x & 31u, slot = lane / L, v = lane % L;
+  const uint32_t wib = threadIdx.x >> 5;
+  const uint32_t warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = gridDim.x * WARPS;
+  // per-warp rings: B rows [GST][32][L] (16-byte vectors), col [NA][32], val [NA][32]
+  V* const s_b = reinterpret_cast<V*>(dsm) + size_t(wib) * GST * 32 * L;
+  uint32_t* const s_ci = reinterpret_cast<uint32_t*>(dsm + size_t(WARPS) * GST * 32 * L * 16) +
+                         size_t(wib) * NA * 32;
+  T* const s_val = reinterpret_cast<T*>(dsm + size_t(WARPS) * GST * 32 * L * 16 +
+                                        size_t(WARPS) * NA * 32 * 4) +
+                   size_t(wib) * NA * 32;
+  const bool colok = v < p.nvec;
+  // this lane's 16 bytes of B row 0: a gather adds k * ldb bytes (one
+  // IMAD.WIDE.U32; B rows are < 4 GB)
+  const uint32_t vb = (colok ? v : 0) * 16u;
+  const char* const Blane = reinterpret_cast<const char*>(p.B) + vb;
+  const uint32_t ldbb = uint32_t(p.ldb * sizeof(T));
+  T* __restrict__ Cs = p.C;
+  uint32_t coff = 0;
+#pragma unroll
+  for (int lv = 0; lv < SCAT; ++lv)
+    if (slot & (1u << lv)) coff += VEC >> (lv + 1);
+  const bool owner = colok && (slot >> SCAT) == 0;
+  const uint32_t col0 = v * VEC + coff;
+  constexpr unsigned full = 0xffffffffu;
+  // positions fit in 32 bits: row_ptr is uint32 (tile.hpp:17)
+  const uint32_t nnz = uint32_t(p.nnz), Q = uint32_t(p.Q), nch = p.nchunks;
+  auto chunk_hi = [&](uint32_t lo) { return nnz - lo > Q ? lo + Q : nnz; };
+
+  // issue sides: (chunk, window start, chunk end) of the next col/val window
+  // and of the next gather batch, walking the warp's chunks in order
+  uint32_t iac = warp, iaw = warp * Q, iah = warp < nch ? chunk_hi(warp * Q) : 0;
+  uint32_t igc = warp, igw = iaw, igh = iah;
+  uint32_t na = 0, ng = 0, ga = 0;
+  // a window is stored slot-major ([S][U]: position u*S + s at s*U + u) so a
+  // lane reads the U col/val entries of its slot as whole vectors
+  const uint32_t adst = (lane % S) * U + lane / S;
+  auto issue_a = [&]() {
+    if (iac < nch) {
+      const uint32_t idx = iaw + lane;
+      const bool ok = idx < iah;
+      cp_async(&s_ci[na * 32 + adst], p.ci + (ok ? idx : 0), ok, 4);
+      cp_async(&s_val[na * 32 + adst], p.val + (ok ? idx : 0), ok, int(sizeof(T)));
+      iaw += 32;
+      if (iaw >= iah) {
+        iac += nwarps;
+        iaw = iac * Q;
+        iah = iac < nch ? chunk_hi(iaw) : 0;
+      }
+    }
+    na = na + 1 == NA ? 0 : na + 1;
+  };
+  auto gsrc = [&](uint32_t k) -> const void* {
+    if constexpr (SEG) {
+      const uint32_t sg = p.seg_shift < 32 ? (k >> p.seg_shift) : (k / p.seg_rows);
+      const uint32_t r = k - sg * p.seg_rows;
+      return reinterpret_cast<const char*>(segs.base[sg]) + vb + uint64_t(r) * ldbb;
+    } else {
+      return Blane + uint64_t(k) * ldbb;
+    }
+  };
+  auto issue_g = [&]() {
+    if (igc < nch) {
+      uint32_t kk[U];
+      lds_vec<U>(kk, s_ci + ga * 32 + slot * U);
+      V* dst = s_b + size_t(ng) * 32 * L + lane;
+      if (igw + 32 <= igh) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) cp_async16(dst + u * 32, gsrc(kk[u]), colok);
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          cp_async16(dst + u * 32, gsrc(kk[u]), colok && igw + uint32_t(u * S) + slot < igh);
+      }
+      igw += 32;
+      if (igw >= igh) {
+        igc += nwarps;
+        igw = igc * Q;
+        igh = igc < nch ? chunk_hi(igw) : 0;
+      }
+    }
+    ng = ng + 1 == GST ? 0 : ng + 1;
+    ga = ga + 1 == NA ? 0 : ga + 1;
+  };
+  // prologue: D col/val windows (one group each), then GST-1 gather batches
+#pragma unroll 1
+  for (int q = 0; q < D; ++q) {
+    issue_a();
+    cp_async_commit();
+  }
+  cp_async_wait<D - GST>();
+  __syncwarp();
+#pragma unroll 1
+  for (int q = 0; q < GST - 1; ++q) {
+    issue_g();
+    cp_async_commit();
+  }
+
+  auto reduce = [&](const V& acc, T (&out)[LEN]) {
+    T r[VEC];
+    const T* pa = reinterpret_cast<const T*>(&acc);
+#pragma unroll
+    for (int x = 0; x < VEC; ++x) r[x] = pa[x];
+#pragma unroll
+    for (int lv = 0; lv < LOGS; ++lv) {
+      const int off = L << lv;
+      if (lv < SCAT) {
+        const int half = VEC >> (lv + 1);
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int x = 0; x < VEC / 2; ++x) {
+          if (x < half) {
+            const T send = upper ? r[x] : r[x + half];
+            const T keep = upper ? r[x + half] : r[x];
+            r[x] = keep + __shfl_xor_sync(full, send, off);
+          }
+        }
+      } else {
+        r[0] += __shfl_xor_sync(full, r[0], off);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < LEN; ++x) out[x] = r[x];
+  };
+
+  uint32_t ca = 0, cg = 0;  // consume-side ring slots
+  uint32_t nrow = warp < nch ? __ldg(p.chunk_row + warp) : 0;
+  for (uint32_t c = warp; c < nch; c += nwarps) {
+    const uint32_t lo = c * Q, hi = chunk_hi(lo);
+    uint32_t row = nrow, rb = row;
+    uint32_t rew = rb + lane < p.rows ? __ldg(p.rp + rb + lane + 1) : 0xFFFFFFFFu;
+    bool starts = __ldg(p.rp + row) >= lo;
+    if (c + nwarps < nch) nrow = __ldg(p.chunk_row + c + nwarps);
+    uint32_t rend = __shfl_sync(full, rew, 0);
+    uint32_t rstart = lo;
+    V acc = vzero<V>();
+    T cin[LEN];
+    T* crow = Cs + uint64_t(row) * p.ldc + col0;
+#pragma unroll
+    for (int x = 0; x < LEN; ++x) cin[x] = (!CZERO && starts && owner) ? __ldcs(crow + x) : T(0);
+    // flush the current row (it ends at rend) and move to the next one
+    auto flush = [&]() {
+      T o[LEN];
+      reduce(acc, o);
+      if (owner) {
+        if (starts) {
+#pragma unroll
+          for (int x = 0; x < LEN; ++x) __stcs(crow + x, CZERO ? o[x] : cin[x] + o[x]);
+        } else {
+#pragma unroll
+          for (int x = 0; x < LEN; ++x) p.head_val[uint64_t(c) * p.wstride + col0 + x] = o[x];
+        }
+      }
+      rstart = rend;
+      for (;;) {  // next row holding position rstart (skips empty rows)
+        const uint32_t d = __popc(__ballot_sync(full, rew <= rstart));
+        if (d < 32u) {
+          row = rb + d;
+          rend = __shfl_sync(full, rew, d);
+          break;
+        }
+        rb += 32;
+        rew = rb + lane < p.rows ? __ldg(p.rp + rb + lane + 1) : 0xFFFFFFFFu;
+      }
+      starts = true;
+      acc = vzero<V>();
+      crow = Cs + uint64_t(row) * p.ldc + col0;
+#pragma unroll
+      for (int x = 0; x < LEN; ++x) cin[x] = (!CZERO && owner) ? __ldcs(crow + x) : T(0);
+    };
+    for (uint32_t w = lo; w < hi; w += 32) {
+      issue_a();
+      issue_g();
+      cp_async_commit();
+      cp_async_wait<GST - 1>();
+      __syncwarp();
+      T aw[U];
+      lds_vec<U>(aw, s_val + ca * 32 + slot * U);
+      const V* bw = s_b + size_t(cg) * 32 * L + lane;
+      if (rend >= w + 32 && w + 32 <= hi) {
+        // the whole batch lies inside the current row
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = vfma(aw[u], bw[u * 32], acc);
+      } else if (w + 32 <= hi) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t base = w + uint32_t(u * S);
+          const T a = aw[u];
+          const V b = bw[u * 32];
+          if (rend >= base + S) {
+            acc = vfma(a, b, acc);
+          } else {
+            const uint32_t pos = base + slot;
+            do {
+              if (pos >= rstart && pos < rend) acc = vfma(a, b, acc);
+              flush();
+            } while (rend < base + S);
+            if (pos >= rstart) acc = vfma(a, b, acc);
+          }
+        }
+      } else {
+        // the chunk's last, partial batch
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t base = w + uint32_t(u * S);
+          if (base >= hi) break;
+          const T a = aw[u];
+          const V b = bw[u * 32];
+          const uint32_t pos = base + slot;
+          const bool valid = pos < hi;
+          const uint32_t lim = min(base + S, hi);
+          while (rend < lim) {
+            if (valid && pos >= rstart && pos < rend) acc = vfma(a, b, acc);
+            flush();
+          }
+          if (valid && pos >= rstart) acc = vfma(a, b, acc);
+        }
+      }
+      __syncwarp();
+      ca = ca + 1 == NA ? 0 : ca + 1;
+      cg = cg + 1 == GST ? 0 : cg + 1;
+    }
+    T o[LEN];
+    reduce(acc, o);
+    if (!CZERO && starts)
+#pragma unroll
+      for (int x = 0; x < LEN; ++x) o[x] = cin[x] + o[x];
+    int32_t trow = -1;
+    if (rend <= hi && starts) {
+      if (owner)
+#pragma unroll
+        for (int x = 0; x < LEN; ++x) __stcs(crow + x, o[x]);
+    } else {
+      if (owner)
+#pragma unroll
+        for (int x = 0; x < LEN; ++x)
+          (starts ? p.tail_val : p.head_val)[uint64_t(c) * p.wstride + col0 + x] = o[x];
+      if (starts) trow = int32_t(row);
+    }
+    if (lane == 0) p.tail_row[c] = trow;
+  }
+  cp_async_wait<0>();
+}
+
 // Row-oriented variant: the worker walks the chunk row by row; each row
 // (or the chunk's slice of it) is accumulated from its own col/val window.
 template <typename T, int VEC, int G, int NV, bool CZERO, int MINB, bool SEG>
@@ -358,14 +1021,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   for (uint32_t c = worker; c < p.nchunks; c += nworkers) {
     const uint64_t lo = uint64_t(c) * p.Q;
     const uint64_t hi = umin(lo + p.Q, p.nnz);
-    uint32_t l = 0, h = p.rows;
-    while (h - l > 1) {
-      const uint32_t m = (l + h) >> 1;
-      if (__ldg(p.rp + m) <= lo)
-        l = m;
-      else
-        h = m;
-    }
+    const uint32_t l = __ldg(p.chunk_row + c);
     uint32_t r = l;
     uint32_t rs = __ldg(p.rp + r);
     uint32_t re = __ldg(p.rp + r + 1);
@@ -467,14 +1123,7 @@ __global__ void __launch_bounds__(kThreads)
   for (uint32_t c = warp; c < p.nchunks; c += nwarps) {
     const uint64_t lo = uint64_t(c) * p.Q;
     const uint64_t hi = umin(lo + p.Q, p.nnz);
-    uint32_t l = 0, h = p.rows;
-    while (h - l > 1) {
-      const uint32_t m = (l + h) >> 1;
-      if (__ldg(p.rp + m) <= lo)
-        l = m;
-      else
-        h = m;
-    }
+    const uint32_t l = __ldg(p.chunk_row + c);
     uint32_t r = l;
     uint32_t rs = __ldg(p.rp + r), re = __ldg(p.rp + r + 1);
     int32_t trow = -1;
@@ -570,39 +1219,69 @@ __global__ void __launch_bounds__(kThreads) spmm_fixup(const SpmmArgs<T> p) {
   }
 }
 
-// RDMM_SPMM_KERNEL=rows|stream forces a kernel (dev switch; default auto;
-// narrow rows accept only "rows").
+// RDMM_SPMM_KERNEL=rows|stream|vec forces a kernel family (a measurement
+// switch; default auto).
 inline int kernel_variant() {
   static const int v = [] {
     const char* e = std::getenv("RDMM_SPMM_KERNEL");
     if (!e) return 0;  // auto
-    return std::string(e) == "rows" ? 1 : 2;
+    const std::string s(e);
+    return s == "rows" ? 1 : s == "stream" ? 2 : s == "vec" ? 3 : 0;
   }();
   return v;
 }
 
+// RDMM_SPMM_ASYNC=0 disables the cp.async-gather narrow kernel (rows of at
+// most 128 bytes).  A measurement switch.
+inline bool async_mode() {
+  static const bool v = [] {
+    const char* e = std::getenv("RDMM_SPMM_ASYNC");
+    return !(e && std::string(e) == "0");
+  }();
+  return v;
+}
+
+// Kernel choice, measured on B200 (profiles/):
+//  * narrow rows (nvec < 32 vectors: N < 128 fp32) -> spmm_slots, the warp
+//    streaming one nnz chunk with S = 32/L slots (N = 32 on cfg3's A:
+//    spmm_vec 2.82 ms, per-group spmm_stream 2.08 ms);
+//  * one 16-B vector per lane (N = 128 fp32) -> spmm_stream at 64 registers,
+//    4 CTAs/SM;
+//  * wider rows (NV >= 2 vectors per lane) -> spmm_rows, at the HBM gather
+//    roofline on ER (cfg5).
 template <typename T, int VEC, int G, int NV, bool SEG>
 void launch_seg(const SpmmArgs<T>& a, bool czero, int blocks, cudaStream_t s) {
-  // Measured on B200 (profiles/): the nnz-stream kernel at
-  // 64 registers (4 CTAs/SM) wins for one 16-B vector per lane (N=128 fp32);
-  // wider rows (NV>=2) keep more gathers in flight per lane and the
-  // row-oriented kernel is faster there (at the HBM gather roofline on ER);
-  // narrow rows (N<128) use the whole-warp row kernel.
-  // Only the (kernel, occupancy) pairs that a setting can select are
-  // instantiated: narrow rows -> spmm_vec (or spmm_rows when forced);
-  // G=32,NV=1 -> 4 CTAs/SM; wider -> 1 CTA/SM minimum.
   const int kv = kernel_variant();
   if constexpr (G < 32) {
-    if (kv == 1) {
+    constexpr int S = 32 / G;
+    constexpr bool v16 = sizeof(typename VecOf<T, VEC>::type) <= 16;
+    if constexpr (!v16) {  // 32-byte vectors: spmm_slots only
+      if (czero) spmm_slots<T, VEC, S, true, 3, SEG><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_slots<T, VEC, S, false, 3, SEG><<<blocks, kThreads, 0, s>>>(a);
+    } else if (kv == 0 && G <= 8 && VEC * sizeof(T) == 16 && async_mode()) {
+      const size_t sm = AsyncCfg<T>::smem(G);
+      auto fn = czero ? spmm_slots_async<T, S, true, SEG> : spmm_slots_async<T, S, false, SEG>;
+      static int resident[2] = {0, 0};  // CTAs per SM (persistent grid)
+      if (!resident[czero]) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        int nb = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, sm);
+        resident[czero] = nb > 0 ? nb : 1;
+      }
+      fn<<<std::min(blocks, resident[czero] * num_sms()), kThreads, sm, s>>>(a);
+    } else if (kv == 1) {
       if (czero) spmm_rows<T, VEC, G, NV, true, 1, SEG><<<blocks, kThreads, 0, s>>>(a);
       else spmm_rows<T, VEC, G, NV, false, 1, SEG><<<blocks, kThreads, 0, s>>>(a);
-    } else {
+    } else if (kv == 3) {
       if (czero) spmm_vec<T, VEC, G, true, SEG><<<blocks, kThreads, 0, s>>>(a);
       else spmm_vec<T, VEC, G, false, SEG><<<blocks, kThreads, 0, s>>>(a);
+    } else {
+      if (czero) spmm_slots<T, VEC, S, true, 3, SEG><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_slots<T, VEC, S, false, 3, SEG><<<blocks, kThreads, 0, s>>>(a);
     }
   } else {
     constexpr int MB = NV == 1 ? 4 : 1;
-    const bool use_rows = kv == 1 || (kv == 0 && NV != 1);
+    const bool use_rows = kv == 1 || (kv != 2 && NV != 1);
     if (use_rows) {
       if (czero) spmm_rows<T, VEC, G, NV, true, MB, SEG><<<blocks, kThreads, 0, s>>>(a);
       else spmm_rows<T, VEC, G, NV, false, MB, SEG><<<blocks, kThreads, 0, s>>>(a);
@@ -642,6 +1321,19 @@ void dispatch(const SpmmArgs<T>& a, bool cz, int G, int NV, int blocks,
   }
 }
 
+// 32-byte vectors: narrow rows only (G < 32, spmm_slots)
+template <typename T, int VEC>
+void dispatch_narrow(const SpmmArgs<T>& a, bool cz, int G, int blocks, int fix_blocks,
+                     cudaStream_t s) {
+  switch (G) {
+    case 1: launch<T, VEC, 1, 1>(a, cz, blocks, fix_blocks, s); break;
+    case 2: launch<T, VEC, 2, 1>(a, cz, blocks, fix_blocks, s); break;
+    case 4: launch<T, VEC, 4, 1>(a, cz, blocks, fix_blocks, s); break;
+    case 8: launch<T, VEC, 8, 1>(a, cz, blocks, fix_blocks, s); break;
+    default: launch<T, VEC, 16, 1>(a, cz, blocks, fix_blocks, s); break;
+  }
+}
+
 constexpr int kMaxNV = 4;
 
 // Panel width in vectors handled by one launch pair.
@@ -668,41 +1360,58 @@ inline int groups_for(uint32_t nvec, int* NV) {
 }
 
 struct SpmmPlan {
-  int VEC = 1, blocks = 0, fix_blocks = 0;
+  int VEC = 1, blocks = 0, fix_blocks = 0, chunk_blocks = 0;
   uint32_t pv = 0, nchunks = 0, wstride = 0;
   uint64_t Q = 0;
   size_t bytes = 0;
 };
 
+// RDMM_SPMM_V32=0 disables the 32-byte-vector narrow path; =all extends it to
+// rows of 512 bytes (N = 128 fp32).  A measurement switch.
+inline int v32_mode() {
+  static const int v = [] {
+    const char* e = std::getenv("RDMM_SPMM_V32");
+    if (!e) return 1;
+    const std::string s(e);
+    return s == "0" ? 0 : s == "all" ? 2 : 1;
+  }();
+  return v;
+}
+
+// vmode: 0 scalar, 1 16-byte vectors, 2 32-byte vectors (narrow rows only)
 template <typename T>
-SpmmPlan make_plan(uint64_t nnz, uint32_t n, bool vec_ok) {
+SpmmPlan make_plan(uint32_t rows, uint64_t nnz, uint32_t n, int vmode) {
   constexpr int VV = sizeof(T) == 4 ? 4 : 2;
   SpmmPlan P;
-  P.VEC = vec_ok ? VV : 1;
+  P.VEC = vmode == 2 ? 2 * VV : vmode == 1 ? VV : 1;
   const uint32_t nvec_total = n / P.VEC;
   const int sms = num_sms();
   P.pv = std::min<uint32_t>(nvec_total, panel_vecs());
   int NV = 1;
   const int G = groups_for(P.pv, &NV);
+  // a worker is a warp (spmm_slots / spmm_stream / spmm_rows at G = 32), or
+  // a G-lane group for the forced narrow row kernels
+  const int wl = (G < 32 && kernel_variant() == 0) ? 32 : G;
   const int blocks_max = sms * 8;  // 8 x 256 threads per SM (register bound)
-  const uint32_t per_block = kThreads / G;
+  const uint32_t per_block = kThreads / wl;
   const uint32_t workers = uint32_t(blocks_max) * per_block;
   const uint32_t nchunks = chunk_count(std::max<uint64_t>(nnz, 1), workers);
   P.Q = ceil_div(std::max<uint64_t>(nnz, 1), nchunks);
   P.nchunks = uint32_t(ceil_div(std::max<uint64_t>(nnz, 1), P.Q));
   P.wstride = uint32_t(ceil_div(uint64_t(P.pv) * P.VEC, 4) * 4);
-  P.bytes = 2 * size_t(P.nchunks) * P.wstride * sizeof(T) +
-            size_t(P.nchunks) * 4 + 256;
+  P.bytes = 2 * size_t(P.nchunks) * P.wstride * sizeof(T) + 2 * size_t(P.nchunks) * 4 + 256;
   P.blocks = int(std::min<uint64_t>(blocks_max, ceil_div(P.nchunks, per_block)));
-  P.fix_blocks = int(std::min<uint64_t>(sms * 4, ceil_div(P.nchunks, per_block)));
+  P.fix_blocks = int(std::min<uint64_t>(sms * 4, ceil_div(P.nchunks, kThreads / G)));
+  P.chunk_blocks = int(std::max<uint64_t>(
+      1, std::min<uint64_t>(uint64_t(sms) * 8, ceil_div(uint64_t(rows), kThreads))));
   return P;
 }
 
 template <typename T>
 size_t workspace_bytes_impl(uint32_t rows, uint64_t nnz, uint32_t n) {
-  (void)rows;
-  return std::max(make_plan<T>(nnz, n, true).bytes,
-                  make_plan<T>(nnz, n, false).bytes);
+  size_t b = 0;
+  for (int vm = 0; vm < 3; ++vm) b = std::max(b, make_plan<T>(rows, nnz, n, vm).bytes);
+  return b;
 }
 
 template <typename T>
@@ -721,13 +1430,22 @@ int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
   cudaStream_t s = as_stream(stream);
   constexpr int VV = sizeof(T) == 4 ? 4 : 2;
   if (nseg > 16) return fail(RDMM_ERR_INVALID, "spmm: at most 16 B segments");
-  bool seg_aligned = true;
-  for (uint32_t q = 0; q < nseg; ++q)
-    seg_aligned &= (reinterpret_cast<uintptr_t>(bseg[q]) % 16) == 0;
-  const bool vec_ok = n % VV == 0 && ldb % VV == 0 && ldc % VV == 0 &&
-                      (nseg ? seg_aligned : (reinterpret_cast<uintptr_t>(B) % 16) == 0) &&
-                      (reinterpret_cast<uintptr_t>(C) % 16) == 0;
-  const SpmmPlan P = make_plan<T>(nnz, n, vec_ok);
+  auto aligned = [&](uintptr_t a) {
+    bool ok = (reinterpret_cast<uintptr_t>(C) % a) == 0;
+    if (nseg)
+      for (uint32_t q = 0; q < nseg; ++q) ok &= (reinterpret_cast<uintptr_t>(bseg[q]) % a) == 0;
+    else
+      ok &= (reinterpret_cast<uintptr_t>(B) % a) == 0;
+    return ok;
+  };
+  const bool vec_ok = n % VV == 0 && ldb % VV == 0 && ldc % VV == 0 && aligned(16);
+  // 32-byte vectors for narrow rows (<= 256 bytes; <= 512 with RDMM_SPMM_V32=all)
+  const uint64_t max_row = v32_mode() == 2 ? 512 : 256;
+  const bool async_rows = async_mode() && kernel_variant() == 0 && uint64_t(n) * sizeof(T) <= 128;
+  const bool v32_ok = !async_rows && v32_mode() != 0 && kernel_variant() == 0 && n % (2 * VV) == 0 &&
+                      ldb % (2 * VV) == 0 && ldc % (2 * VV) == 0 && aligned(32) &&
+                      uint64_t(n) * sizeof(T) <= max_row;
+  const SpmmPlan P = make_plan<T>(rows, nnz, n, v32_ok ? 2 : vec_ok ? 1 : 0);
   void* w = ws;
   if (!w || ws_bytes < P.bytes) {
     if (ws) return fail(RDMM_ERR_INVALID, "spmm: workspace too small");
@@ -758,8 +1476,12 @@ int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
   a.head_val = reinterpret_cast<T*>(base);
   a.tail_val = reinterpret_cast<T*>(base + vbytes);
   a.tail_row = reinterpret_cast<int32_t*>(base + 2 * vbytes);
+  uint32_t* chunk_row = reinterpret_cast<uint32_t*>(base + 2 * vbytes + size_t(P.nchunks) * 4);
+  a.chunk_row = chunk_row;
   const uint32_t nvec_total = n / P.VEC;
   KernelTimer timer(s, 1);
+  count_launch(1);
+  spmm_chunk_rows<<<P.chunk_blocks, kThreads, 0, s>>>(rp, rows, P.Q, P.nchunks, chunk_row);
   for (uint32_t v0 = 0; v0 < nvec_total; v0 += P.pv) {
     count_launch(2);
     const uint32_t nv = std::min<uint32_t>(P.pv, nvec_total - v0);
@@ -771,8 +1493,10 @@ int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
     a.nvec = nv;
     if (P.VEC == 1)
       dispatch<T, 1>(a, czero, g, nvp, P.blocks, P.fix_blocks, s);
-    else
+    else if (P.VEC == VV)
       dispatch<T, VV>(a, czero, g, nvp, P.blocks, P.fix_blocks, s);
+    else
+      dispatch_narrow<T, 2 * VV>(a, czero, g, P.blocks, P.fix_blocks, s);
   }
   RDMM_CUDA_TRY(cudaGetLastError());
   return RDMM_OK;

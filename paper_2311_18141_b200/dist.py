@@ -26,7 +26,7 @@ class Options(C.Structure):
                 ("random_delay_ms_max", C.c_double), ("record_events", C.c_int),
                 ("record_triples", C.c_int), ("lookahead", C.c_int),
                 ("ws_local_inplace", C.c_int), ("checksum", C.c_int), ("fuse_k", C.c_int),
-                ("split_local", C.c_int)]
+                ("split_local", C.c_int), ("time_stages", C.c_int)]
 
 
 class Report(C.Structure):
@@ -38,7 +38,7 @@ class Report(C.Structure):
                                          "bytes_on_node", "bytes_off_node")] + [
         ("total_seconds", C.c_double * MAXR), ("ntriples", C.c_uint64),
         ("triples", C.POINTER(C.c_uint32)), ("nstages", C.c_uint32),
-        ("stage_flops", C.POINTER(C.c_uint64))]
+        ("stage_flops", C.POINTER(C.c_uint64)), ("stage_ms", C.POINTER(C.c_double))]
 
 
 _u32, _u64, _vp, _int = C.c_uint32, C.c_uint64, C.c_void_p, C.c_int
@@ -77,6 +77,15 @@ for _n in ("rdmm_h_fabric_create", "rdmm_h_matrix_create", "rdmm_h_sparse_init",
            "rdmm_h_dense_init", "rdmm_h_dense_to_host", "rdmm_h_sparse_nnz",
            "rdmm_h_sparse_to_host", "rdmm_h_run_multiply"):
     getattr(_h, _n).restype = _int
+
+
+class TrafficRec(C.Structure):  # rdmm_traffic (fabric.hpp:89-203 TrafficLog cell)
+    _fields_ = [("bytes_put", C.c_uint64), ("bytes_got", C.c_uint64), ("puts", C.c_uint64),
+                ("gets", C.c_uint64), ("atomic_ops", C.c_uint64)]
+
+
+_h.rdmm_traffic_pair.argtypes = [_vp, _u32, _u32, C.POINTER(TrafficRec)]
+_h.rdmm_traffic_pair.restype = _int
 
 
 class TileFetchRec(C.Structure):
@@ -128,6 +137,26 @@ class Fabric:
         arr = (TileFetchRec * max(1, n))()
         _h.rdmm_tile_fetches(self.handle, arr, n)
         return [(r.src, r.dst, r.label, r.matrix, r.i, r.j) for r in arr[:n]]
+
+    def traffic(self, src, dst):
+        """Bytes and operations moved from rank `src` to rank `dst` as logged
+        by this process (gets issued by dst, puts issued by src): the byte-exact
+        TrafficLog of fabric.hpp:89-203."""
+        t = TrafficRec()
+        L.check(_h.rdmm_traffic_pair(self.handle, src, dst, C.byref(t)), "traffic")
+        return dict(bytes_put=t.bytes_put, bytes_got=t.bytes_got, puts=t.puts, gets=t.gets,
+                    atomic_ops=t.atomic_ops)
+
+    def remote_bytes_in(self, rank):
+        """Bytes `rank` received from other ranks (NVLink traffic into its GPU):
+        its gets from peers plus peers' puts into it, as logged here."""
+        tot = 0
+        for r in range(self.nranks):
+            if r == rank:
+                continue
+            t = self.traffic(r, rank)
+            tot += t["bytes_got"] + t["bytes_put"]
+        return tot
 
     def clear_traffic(self):
         _h.rdmm_traffic_clear(self.handle)
@@ -278,6 +307,8 @@ class RunReport:
     triples: list = field(default_factory=list)
     # flops per rank per k tile step (RankStats::stage_flops), int64 [P, K]
     stage_flops: np.ndarray = field(default_factory=lambda: np.zeros((0, 0), np.int64))
+    # device ms per rank per k tile step (RankStats::stage_ms, time_stages=True)
+    stage_ms: np.ndarray | None = None
 
     def imbalance(self):
         """Per-stage and end-to-end flop imbalance of this run
@@ -290,12 +321,12 @@ def run_multiply(f: Fabric, A: DistSparse, B, Cm, variant="stationary_c", ws_bas
                  prefetch=True, offset=True, seed=0, delay_ns_per_flop=0.0,
                  random_delay_ms_max=0.0, record_events=True, record_triples=False,
                  lookahead=2, ws_local_inplace=True, checksum=True, fuse_k=True,
-                 split_local=True) -> RunReport:
+                 split_local=True, time_stages=False) -> RunReport:
     """C += A*B on the fabric -- algos.hpp:673-752."""
     o = Options(VARIANTS.index(variant), VARIANTS.index(ws_base), int(prefetch), int(offset),
                 seed, delay_ns_per_flop, random_delay_ms_max, int(record_events),
                 int(record_triples), lookahead, int(ws_local_inplace), int(checksum),
-                int(fuse_k), int(split_local))
+                int(fuse_k), int(split_local), int(time_stages))
     r = Report()
     L.check(_h.rdmm_h_run_multiply(f._h, A._h, B._h, Cm._h, C.byref(o), C.byref(r)),
             "run_multiply")
@@ -316,5 +347,10 @@ def run_multiply(f: Fabric, A: DistSparse, B, Cm, variant="stationary_c", ws_bas
         sf[:] = np.ctypeslib.as_array(r.stage_flops, shape=(r.nranks * r.nstages,)).reshape(
             r.nranks, r.nstages)
         _h.rdmm_h_free(r.stage_flops)
+    sm = None
+    if r.nstages and r.stage_ms:
+        sm = np.ctypeslib.as_array(r.stage_ms, shape=(r.nranks * r.nstages,)).reshape(
+            r.nranks, r.nstages).copy()
+        _h.rdmm_h_free(r.stage_ms)
     return RunReport(r.wall_seconds, r.checksum, r.total_flops, r.total_multiplies,
-                     r.total_steals, per, tr, sf)
+                     r.total_steals, per, tr, sf, sm)

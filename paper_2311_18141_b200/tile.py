@@ -94,8 +94,7 @@ class DeviceCsr:
 
 
 def spmm_local(a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, stream=None,
-               workspace: torch.Tensor | None = None, c_zero: bool = False,
-               prefetch: bool = True) -> FlopMeter:
+               workspace: torch.Tensor | None = None, c_zero: bool = False) -> FlopMeter:
     """c += a @ b on the device; tile.hpp:170-188.  Raises DimensionError on
     mismatch exactly like the reference (tile.hpp:173-174).  c_zero=True
     asserts c is all-zero on entry (it is then written, never read)."""
@@ -109,7 +108,7 @@ def spmm_local(a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, stream=None,
     fl = C.c_uint64(0)
     ws = workspace.data_ptr() if workspace is not None else None
     wsb = workspace.numel() * workspace.element_size() if workspace is not None else 0
-    flags = (L.SPMM_C_ZERO if c_zero else 0) | (0 if prefetch else L.SPMM_NO_PREFETCH)
+    flags = L.SPMM_C_ZERO if c_zero else 0
     L.check(L.rdmm_spmm_csr_ex(_wcode(a.dtype), a.rows, a.cols, n, a.nnz, a.row_ptr.data_ptr(),
                                a.col_idx.data_ptr(), a.values.data_ptr(), b.data_ptr(),
                                b.stride(0), c.data_ptr(), c.stride(0), flags, ws, wsb,

@@ -1,5 +1,7 @@
-"""Time spmm_local on a BASELINE config (dev tool; env vars select kernel
-variants: RDMM_SPMM_PREFETCH, RDMM_SPMM_KERNEL)."""
+"""Time spmm_local on a BASELINE-shaped input (dev tool).  Kernel-family and
+chunking switches come from the environment (RDMM_SPMM_KERNEL=rows|stream|vec,
+RDMM_SPMM_CPW); the printed `bits` (sum of the fp32 bit patterns of C) lets
+runs with different switches be compared for bitwise-identical results."""
 import argparse
 import json
 import os
@@ -13,7 +15,7 @@ import paper_2311_18141_b200 as rd  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=22)
 ap.add_argument("--ef", type=int, default=16)
-ap.add_argument("--n", type=int, default=128)
+ap.add_argument("--n", type=int, nargs="+", default=[128])
 ap.add_argument("--er", action="store_true")
 ap.add_argument("--czero", type=int, default=0)
 ap.add_argument("--iters", type=int, default=20)
@@ -23,19 +25,25 @@ if args.er:
     a = rd.uniform_tiles(1 << args.scale, 1 << args.scale, 1, 16.0 / (1 << args.scale), 1)
 else:
     a = rd.rmat(args.scale, args.ef, seed=1)
-b = rd.random_dense(a.cols, args.n, 2)
-c = torch.zeros((a.rows, args.n), device="cuda")
-for _ in range(3):
-    rd.spmm_local(a, b, c, c_zero=bool(args.czero))
-torch.cuda.synchronize()
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record()
-for _ in range(args.iters):
-    rd.spmm_local(a, b, c, c_zero=bool(args.czero))
-e1.record()
-torch.cuda.synchronize()
-ms = e0.elapsed_time(e1) / args.iters
-fl = 2 * a.nnz * args.n
-print(json.dumps({"tag": args.tag, "ms": ms, "gflops": fl / ms / 1e6,
-                  "env": {k: v for k, v in os.environ.items() if k.startswith("RDMM_")},
-                  "czero": args.czero, "scale": args.scale, "n": args.n, "er": args.er}))
+for n in args.n:
+    b = rd.random_dense(a.cols, n, 2)
+    c = torch.zeros((a.rows, n), device="cuda")
+    rd.spmm_local(a, b, c, c_zero=True)
+    torch.cuda.synchronize()
+    bits = int(c.view(torch.int32).long().sum())
+    for _ in range(3):
+        rd.spmm_local(a, b, c, c_zero=bool(args.czero))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.iters):
+        rd.spmm_local(a, b, c, c_zero=bool(args.czero))
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.iters
+    fl = 2 * a.nnz * n
+    print(json.dumps({"tag": args.tag, "ms": ms, "gflops": fl / ms / 1e6, "bits": bits,
+                      "env": {k: v for k, v in os.environ.items() if k.startswith("RDMM_")},
+                      "czero": args.czero, "scale": args.scale, "n": n, "er": args.er}),
+          flush=True)
+    del b, c
