@@ -121,6 +121,64 @@ def row_sample(rp, ci, vv, stride):
     return nrp, ci[keep], vv[keep]
 
 
+def p2p_peak():
+    """Measured peer-copy bandwidth per GPU (tools/p2p_bw.py on this pool's
+    B200s, committed under profiles/); nominal NVLink 5 otherwise."""
+    for name in ("r2_p2p.json", "r1_diag2/p2p.json"):
+        try:
+            best = 0.0
+            with open(os.path.join(ROOT, "profiles", name)) as fh:
+                for ln in fh:
+                    ln = ln.strip()
+                    if ln.startswith("{"):
+                        best = max(best, float(json.loads(ln)["GBps_per_rank"]))
+            if best:
+                return best, f"measured, profiles/{name} (tools/p2p_bw.py)"
+        except Exception:
+            pass
+    return 900.0, "nominal NVLink 5 per direction"
+
+
+def verify(args, cfg, dev, rank, world, A, Cm, grid, tiles, tdist):
+    """Compare the distributed result with the single-GPU kernel on the
+    global operands (itself pinned to the oracle by tests/): SpMM owned C
+    tiles exactly (integer-valued inputs), SpGEMM row_ptr/col_idx/values of
+    the gathered C exactly."""
+    import numpy as np
+    import torch
+    import paper_2311_18141_b200 as rd
+
+    a, b = gen_inputs(cfg, dev, args.permute)
+    tm, tk, tn = tiles
+    ok = True
+    if cfg["kind"] == "spmm":
+        want = torch.zeros((a.rows, b.shape[1]), device=dev)
+        rd.spmm_local(a, b, want, c_zero=True)
+        got = torch.zeros((a.rows, b.shape[1]), dtype=torch.float32).pin_memory()
+        Cm.owned_to_host(got)
+        torch.cuda.synchronize()
+        w = want.cpu()
+        for i in range(-(-a.rows // tm)):
+            for j in range(-(-b.shape[1] // tn)):
+                if grid.owner(i, j) == rank:
+                    sl = (slice(i * tm, (i + 1) * tm), slice(j * tn, (j + 1) * tn))
+                    ok &= bool(torch.equal(got[sl], w[sl]))
+        what = "owned C tiles == single-GPU spmm_local(A, B) (exact, integer data)"
+    else:
+        if rank == 0:
+            c, _ = rd.spgemm_local(a, a)
+            rp, ci, vv = c.to_host()
+            grp, gci, gvv = Cm.to_global()
+            ok = bool(np.array_equal(rp, grp) and np.array_equal(ci, gci) and
+                      np.array_equal(vv, gvv))
+        what = "gathered C row_ptr/col_idx/values == single-GPU spgemm_local(A, A) (exact)"
+    if tdist:
+        t = torch.tensor([0 if ok else 1], device=dev)
+        tdist.all_reduce(t)
+        ok = int(t[0]) == 0
+    return {"ok": ok, "checked": what}
+
+
 def load_traffic(config, kernel, n_gpus):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -132,15 +190,14 @@ def load_traffic(config, kernel, n_gpus):
 def layout(cfg, P, args):
     """ProcGrid and tile sizes for P ranks.
 
-    SpMM: split B/C columns only while each rank keeps >= 128 fp32 columns
-    (cfg5, N = 256: 1 x 2, then 2 x 2 ...), the rest of P splits A/C rows
-    (cfg3, N = 128: P x 1, K = P row tiles of B).  Each rank keeps the
-    full-width nnz-bound stream kernel and runs its
-    local product A(i,i) B(i,0) first while the copy engines fetch the other
-    B tiles over NVLink (stationary-C offset k = (i+j) % K, lookahead 2).
-    A 1 x P grid (column split) replicates A instead but drops every rank to
-    the narrow N/P kernel, whose cost follows the 4M rows it walks, not the
-    nonzeros: measured 2x slower at P = 2 (profiles/README.md).
+    SpMM: a 1 x P grid (B and C split by columns, A by K = P column tiles):
+    every rank computes all rows of A against its N/P columns of B, so the
+    work is balanced whatever R-MAT's row skew (rank 0 of a P x 1 row split
+    holds 0.733^log2(P) of the nonzeros), only A's tiles cross NVLink
+    ((P-1)/P of A per rank: 402 MB at P = 4 on cfg3) and B stays
+    put.  It needs the narrow-row kernel (spmm_slots_async: N = 32 on cfg3's
+    A in 1.12 ms); columns are split while every rank keeps
+    >= 16 of them.
     SpGEMM: a square-ish pr x pc grid with 4 pr row tiles of C and K = pr
     (cfg2 stationary-C, cfg4 ws_locality): at 4 GPUs 2x2 beats 4x1 by 1.25x
     (cfg2) and 1.44x (cfg4), profiles/r1_s5, r1_s9.
@@ -153,10 +210,7 @@ def layout(cfg, P, args):
         pc = max(d for d in range(1, int(P ** 0.5) + 1) if P % d == 0)
         pr = P // pc
     else:
-        # split columns only while every rank keeps >= 128 fp32 columns
-        pc = 1
-        while cfg["kind"] == "spmm" and P % (2 * pc) == 0 and cfg["n"] // (2 * pc) >= 128:
-            pc *= 2
+        pc = max(d for d in range(1, P + 1) if P % d == 0 and cfg["n"] // d >= 16)
         pr = P // pc
     mt = args.mtiles or (pr if cfg["kind"] == "spmm" else 4 * pr)
     kt = args.ktiles or (max(pr, pc) if cfg["kind"] == "spmm" else pr)
@@ -243,7 +297,8 @@ def run_ours(args, cfg, dev, rank, world):
     import paper_2311_18141_b200 as rd
     import paper_2311_18141_b200.dist as dm
     from paper_2311_18141_b200 import _lib as L
-    from paper_2311_18141_b200.analytics import imbalance_from_flops
+    import numpy as np
+    from paper_2311_18141_b200.analytics import imbalance_from_flops, imbalance_from_times
 
     tdist = torch.distributed if world > 1 else None
     a, b = gen_inputs(cfg, dev, args.permute)
@@ -291,6 +346,7 @@ def run_ours(args, cfg, dev, rank, world):
         reset()
         dm.run_multiply(f, A, B, Cm, **opts)
     torch.cuda.synchronize()
+    f.clear_traffic()
     L.rdmm_kernel_timing(1)
     launches0 = L.rdmm_kernel_launches()
     per, flops_local, steals = [], 0, 0
@@ -313,30 +369,42 @@ def run_ours(args, cfg, dev, rank, world):
     kms, kcount = L.kernel_time(kind_id)
     L.rdmm_kernel_timing(0)
     ms_local = sum(per) / len(per)
-    # per-rank per-k-step flops of the last timed run (RankStats::stage_flops);
-    # rows of ranks hosted by other processes are zero, so a SUM assembles it
-    sf = rep.stage_flops
+    # NVLink bytes into this rank's GPU per step: the fabric's byte-exact
+    # traffic log (gets from peers, contributions read in place)
+    nvl_local = f.remote_bytes_in(rank) / args.steps
+    # Analytics (analytics.hpp:66-90) on one extra, instrumented run outside
+    # the timed loop: the per-rank per-k-step flop table and the per-rank
+    # per-k-step device time of the multiply kernels (cudaEvents on the
+    # compute stream, RunOptions::time_stages).  Rows of ranks hosted by
+    # other processes are zero, so a SUM over processes assembles the tables.
+    reset()
+    barrier()
+    rep_t = dm.run_multiply(f, A, B, Cm, **{**opts, "time_stages": True})
+    torch.cuda.synchronize()
+    barrier()
+    sf = rep_t.stage_flops
+    sm_ = rep_t.stage_ms if rep_t.stage_ms is not None else np.zeros(sf.shape)
     width = torch.tensor([sf.shape[1]], device=dev, dtype=torch.int64)
     if tdist:
         tdist.all_reduce(width, op=tdist.ReduceOp.MAX)
-    table = torch.zeros((sf.shape[0], int(width[0])), device=dev, dtype=torch.float64)
-    table[:, :sf.shape[1]] = torch.as_tensor(sf, dtype=torch.float64)
+    tabs = torch.zeros((2, sf.shape[0], int(width[0])), device=dev, dtype=torch.float64)
+    tabs[0, :, :sf.shape[1]] = torch.as_tensor(sf, dtype=torch.float64)
+    tabs[1, :, :sm_.shape[1]] = torch.as_tensor(sm_, dtype=torch.float64)
     if tdist:
-        tdist.all_reduce(table, op=tdist.ReduceOp.SUM)
-    stage_imb = imbalance_from_flops(table.cpu().numpy())
-    imbalance = {**stage_imb, "definition": "analytics.hpp:66-90 over the run's own "
-                 "per-rank per-k-step flop table"}
-    if tdist:  # per-rank work and time, for the reference's imbalance metrics
-        tt = torch.tensor([ms_local, float(flops_local)], device=dev, dtype=torch.float64)
-        allt = [torch.zeros_like(tt) for _ in range(world)]
-        tdist.all_gather(allt, tt)
-        times = [float(x[0]) for x in allt]
-        works = [float(x[1]) for x in allt]
-        imbalance = {"time_max_over_avg": max(times) / (sum(times) / world),
-                     "flops_max_over_avg": max(works) / max(1e-30, sum(works) / world),
-                     "per_rank_ms": times, **stage_imb,
-                     "definition": "max/avg over ranks (analytics.hpp:58-89 applied to "
-                                   "per-rank device time and FlopMeter work)"}
+        tdist.all_reduce(tabs, op=tdist.ReduceOp.SUM)
+    flop_tab, ms_tab = tabs[0].cpu().numpy(), tabs[1].cpu().numpy()
+    imbalance = {**imbalance_from_flops(flop_tab), **imbalance_from_times(ms_tab),
+                 "per_rank_kernel_ms": [round(float(x), 4) for x in ms_tab.sum(axis=1)],
+                 "definition": "analytics.hpp:66-90 (per-stage = sum_s max_r / sum_s avg_r, "
+                               "end-to-end = max_r / avg_r) over the run's per-rank per-k-step "
+                               "flops and per-rank per-k-step multiply-kernel device time "
+                               "(cudaEvents, RankStats::stage_ms)"}
+    nvlink = None
+    if tdist:  # NVLink bytes per rank per step, against the measured P2P bandwidth
+        nv = torch.tensor([nvl_local], device=dev, dtype=torch.float64)
+        alln = [torch.zeros_like(nv) for _ in range(world)]
+        tdist.all_gather(alln, nv)
+        nvl = [float(x[0]) for x in alln]
     if tdist:  # max over ranks of the device time; flops summed over ranks
         t = torch.tensor([ms_local, float(flops_local), float(steals)], device=dev,
                          dtype=torch.float64)
@@ -345,6 +413,14 @@ def run_ours(args, cfg, dev, rank, world):
         tsum = t[1:].clone()
         tdist.all_reduce(tsum, op=tdist.ReduceOp.SUM)
         ms, total_flops, steals = float(tmax[0]), int(tsum[0]), int(tsum[1])
+        p2p, p2p_src = p2p_peak()
+        nvlink = {"bytes_per_step_per_rank": nvl, "bytes_per_step_total": sum(nvl),
+                  "achieved_gbs_max_rank": max(nvl) / (ms * 1e-3) / 1e9,
+                  "p2p_gbs": p2p, "frac": max(nvl) / (ms * 1e-3) / 1e9 / p2p,
+                  "p2p_source": p2p_src,
+                  "source": "fabric TrafficLog (fabric.hpp:89-203): bytes each rank fetched "
+                            "from peers during the timed steps / step; achieved = busiest "
+                            "rank's bytes over the max-over-ranks step time"}
     else:
         ms, total_flops = ms_local, flops_local
     out_nnz = Cm.nnz() if cfg["kind"] == "spgemm" else None
@@ -450,6 +526,10 @@ def run_ours(args, cfg, dev, rank, world):
     }
     if imbalance:
         out["imbalance"] = imbalance
+    if nvlink:
+        out["nvlink"] = nvlink
+    if args.verify:
+        out["verify"] = verify(args, cfg, dev, rank, world, A, Cm, grid, (tm, tk, tn), tdist)
     # the paper's roofline model (model.hpp:139-160) with B200 costs: local
     # HBM bound and NVLink inter-GPU bound for this shape at N GPUs
     from paper_2311_18141_b200 import model as md
@@ -665,6 +745,21 @@ def run_reference(args):
     }
 
 
+def self_spawn(n):
+    """`bench.py --gpus N` without torchrun: relaunch as one process per GPU
+    (torch.distributed.run on 127.0.0.1) and pass rank 0's line through."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -685,6 +780,8 @@ def main():
     ap.add_argument("--no-fuse", action="store_true", help="RunOptions::fuse_k = false")
     ap.add_argument("--no-split", action="store_true", help="RunOptions::split_local = false")
     ap.add_argument("--lookahead", type=int, default=2, help="RunOptions::lookahead")
+    ap.add_argument("--verify", action="store_true",
+                    help="check the distributed C against the single-GPU kernel")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -698,11 +795,16 @@ def main():
             print(json.dumps(out), flush=True)
         return
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_spawn(args.gpus))
+
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:

@@ -183,9 +183,9 @@ int rdmm_csr_extract_fill(int dtype_bytes, const uint32_t* row_ptr,
                           rdmm_stream_t stream);
 /* Concatenate K (<= 16) CSR tiles of the same rows side by side: tile k's
  * columns are offset by k*col_stride (the A(i,0..K-1) tiles of one tile row
- * -> one CSR for the fused K-tile SpMM).  tile_nnz: host array of the K
- * tiles' nnz (the directory values; NULL = read row_ptr[rows] from the
- * device, which synchronises the stream).  out_rp has rows+1 entries,
+ * -> one CSR for the fused K-tile SpMM).  tile_nnz is accepted for
+ * compatibility and unused (the output row pointer is computed on the
+ * device without a scan or a host round trip).  out_rp has rows+1 entries,
  * out_ci / out_val the sum of the tiles' nnz. */
 int rdmm_csr_concat_cols(int dtype_bytes, uint32_t rows, uint32_t K,
                          const uint32_t* const* row_ptr,
@@ -193,6 +193,14 @@ int rdmm_csr_concat_cols(int dtype_bytes, uint32_t rows, uint32_t K,
                          const void* const* values, const uint64_t* tile_nnz,
                          uint64_t col_stride, uint32_t* out_rp, uint32_t* out_ci,
                          void* out_val, rdmm_stream_t stream);
+/* The same for the block of rows [r0, r0+rows) of the tiles: a standalone
+ * CSR (out_rp[0] = 0) of those rows, e.g. one row block of a pipelined
+ * fused stationary-C step. */
+int rdmm_csr_concat_cols_rows(int dtype_bytes, uint32_t r0, uint32_t rows, uint32_t K,
+                              const uint32_t* const* row_ptr, const uint32_t* const* col_idx,
+                              const void* const* values, uint64_t col_stride,
+                              uint32_t* out_rp, uint32_t* out_ci, void* out_val,
+                              rdmm_stream_t stream);
 /* Sum of a dense tile's values in double (checksum, algos.hpp:634-669). */
 int rdmm_tile_sum(int dtype_bytes, uint32_t rows, uint32_t cols, uint64_t ld,
                   const void* p, rdmm_stream_t stream, double* out);

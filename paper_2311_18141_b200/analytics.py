@@ -33,6 +33,15 @@ def imbalance_from_flops(stage_flops) -> dict:
             "end_to_end_flop_imbalance": _max_over_avg(f.sum(axis=1))}
 
 
+def imbalance_from_times(stage_ms) -> dict:
+    """The same two ratios over a [ranks, stages] table of device time (ms)
+    per rank per k tile step (RankStats::stage_ms, RunOptions::time_stages):
+    the measured counterpart of imbalance_from_flops."""
+    r = imbalance_from_flops(stage_ms)
+    return {"per_stage_time_imbalance": r["per_stage_flop_imbalance"],
+            "end_to_end_time_imbalance": r["end_to_end_flop_imbalance"]}
+
+
 def nnz_imbalance(row_ptr, col_idx, rows, cols, pr, pc) -> float:
     """max/avg nnz over an even pr x pc block split (analytics.hpp:58-64)."""
     return _max_over_avg(block_nnz(row_ptr, col_idx, rows, cols, pr, pc))

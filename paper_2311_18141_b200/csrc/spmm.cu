@@ -100,7 +100,7 @@ __device__ __forceinline__ uint64_t umin(uint64_t a, uint64_t b) {
 __device__ __forceinline__ uint64_t umax(uint64_t a, uint64_t b) {
   return a > b ? a : b;
 }
-// Read-only gather / streaming load / streaming store of one vector.
+// Read-only gather of one vector (256-bit loads for the 32-byte types).
 template <typename V>
 __device__ __forceinline__ V ldg_v(const V* p) {
   return __ldg(p);
@@ -122,37 +122,6 @@ __device__ __forceinline__ double4x ldg_v(const double4x* p) {
                : "l"(p));
   return r;
 }
-template <typename V>
-__device__ __forceinline__ V ldcs_v(const V* p) {
-  return __ldcs(p);
-}
-template <>
-__device__ __forceinline__ float8 ldcs_v(const float8* p) {
-  const float4* q = reinterpret_cast<const float4*>(p);
-  return float8{__ldcs(q), __ldcs(q + 1)};
-}
-template <>
-__device__ __forceinline__ double4x ldcs_v(const double4x* p) {
-  const double2* q = reinterpret_cast<const double2*>(p);
-  return double4x{__ldcs(q), __ldcs(q + 1)};
-}
-template <typename V>
-__device__ __forceinline__ void stcs_v(V* p, V v) {
-  __stcs(p, v);
-}
-template <>
-__device__ __forceinline__ void stcs_v(float8* p, float8 v) {
-  float4* q = reinterpret_cast<float4*>(p);
-  __stcs(q, v.lo);
-  __stcs(q + 1, v.hi);
-}
-template <>
-__device__ __forceinline__ void stcs_v(double4x* p, double4x v) {
-  double2* q = reinterpret_cast<double2*>(p);
-  __stcs(q, v.lo);
-  __stcs(q + 1, v.hi);
-}
-
 template <typename V>
 __device__ __forceinline__ V vzero() {
   V v;

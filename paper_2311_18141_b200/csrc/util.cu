@@ -97,95 +97,92 @@ __device__ __forceinline__ void stage_args(const ConcatArgs& a, ConcatArgs& sa) 
   __syncthreads();
 }
 
-// Row pass: out_rp[r] = sum_k rp_k[r], and for every tile k the shift
-// D_k[r] that moves tile k's nonzero q of row r to its output slot
-// D_k[r] + q, i.e. D_k[r] = sum_{k'<k} rp_k'[r+1] + sum_{k'>k} rp_k'[r].
-constexpr uint32_t kConcatChunk = 2048;
+// Column concatenation of K same-height CSR tiles for a block of rows
+// [r0, r0 + rows): the output row pointer needs no scan, because every
+// tile's row pointer is already a prefix: out_rp[r] = sum_k (rp_k[r0+r] -
+// rp_k[r0]).  One thread per row copies the row's K segments (adjacent rows
+// are adjacent in memory, so a warp's loads and stores stay within a few
+// sectors; thousands of independent rows keep the memory system busy); rows
+// with a segment longer than kLongRow are listed and copied by a warp each.
+constexpr uint32_t kLongRow = 32;
 
-__global__ void k_concat_rows(ConcatArgs a, uint32_t rows, uint32_t* __restrict__ out_rp,
-                              uint32_t* __restrict__ shift, uint32_t* __restrict__ chunk_row,
-                              uint32_t chunk_stride) {
+template <typename T>
+__global__ void k_concat_short(ConcatArgs a, uint32_t r0, uint32_t rows,
+                               uint32_t* __restrict__ out_rp, uint32_t* __restrict__ out_ci,
+                               T* __restrict__ out_val, uint32_t* __restrict__ long_rows,
+                               uint32_t* __restrict__ nlong) {
   __shared__ ConcatArgs sa;
+  __shared__ uint32_t base[16];
   stage_args(a, sa);
+  if (threadIdx.x < sa.K) base[threadIdx.x] = __ldg(sa.rp[threadIdx.x] + r0);
+  __syncthreads();
+  const uint32_t K = sa.K;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r <= rows;
        r += gridDim.x * blockDim.x) {
-    uint32_t total = 0;
-    for (uint32_t k = 0; k < sa.K; ++k) total += __ldg(sa.rp[k] + r);
-    out_rp[r] = total;
-    if (r == rows) continue;
-    uint32_t before = 0;  // sum_{k'<k} rp_k'[r+1]
-    uint32_t after = total;  // sum_{k'>=k} rp_k'[r]
-    for (uint32_t k = 0; k < sa.K; ++k) {
-      const uint32_t s0 = __ldg(sa.rp[k] + r);
-      const uint32_t e0 = __ldg(sa.rp[k] + r + 1);
-      after -= s0;
-      shift[uint64_t(k) * rows + r] = before + after;
-      before += e0;
-      // this row holds the first nonzero of chunks ceil(s0/C) .. (e0-1)/C
-      for (uint32_t c = (s0 + kConcatChunk - 1) / kConcatChunk; e0 > s0 && c <= (e0 - 1) / kConcatChunk;
-           ++c)
-        chunk_row[uint64_t(k) * chunk_stride + c] = r;
+    uint32_t o = 0, maxlen = 0;
+    for (uint32_t k = 0; k < K; ++k) {
+      const uint32_t s0 = __ldg(sa.rp[k] + r0 + r);
+      o += s0 - base[k];
+      if (r < rows) maxlen = max(maxlen, __ldg(sa.rp[k] + r0 + r + 1) - s0);
+    }
+    out_rp[r] = o;
+    if (r == rows || maxlen == 0) continue;
+    if (maxlen > kLongRow) {
+      long_rows[atomicAdd(nlong, 1u)] = r;
+      continue;
+    }
+    for (uint32_t k = 0; k < K; ++k) {
+      const uint32_t s0 = __ldg(sa.rp[k] + r0 + r), e0 = __ldg(sa.rp[k] + r0 + r + 1);
+      const uint32_t off = uint32_t(k * sa.col_stride);
+      const uint32_t* ci = sa.ci[k];
+      const T* val = static_cast<const T*>(sa.val[k]);
+      for (uint32_t t = s0; t < e0; ++t, ++o) {
+        out_ci[o] = __ldg(ci + t) + off;
+        out_val[o] = __ldg(val + t);
+      }
     }
   }
 }
 
-// Element pass for tile k: every warp copies chunks of kConcatChunk
-// consecutive nonzeros (coalesced loads, balanced however long the rows are;
-// the row pass recorded the row of each chunk's first nonzero); the row of
-// each element comes from a 32-row window of row starts held in registers
-// (binary search by shuffles), advanced as the chunk crosses row ends.
 template <typename T>
-__global__ void k_concat_fill(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
-                              const T* __restrict__ val, uint32_t rows, uint32_t off,
-                              const uint32_t* __restrict__ shift,
-                              const uint32_t* __restrict__ chunk_row, uint32_t* __restrict__ out_ci,
-                              T* __restrict__ out_val) {
-  constexpr int U = 4;
+__global__ void k_concat_long(ConcatArgs a, uint32_t r0, const uint32_t* __restrict__ out_rp,
+                              uint32_t* __restrict__ out_ci, T* __restrict__ out_val,
+                              const uint32_t* __restrict__ long_rows,
+                              const uint32_t* __restrict__ nlong) {
+  __shared__ ConcatArgs sa;
+  stage_args(a, sa);
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t nnz = __ldg(rp + rows);
-  const uint32_t nch = (nnz + kConcatChunk - 1) / kConcatChunk;
-  for (uint32_t c = w; c < nch; c += nw) {
-    const uint32_t q0 = c * kConcatChunk;
-    const uint32_t q1 = min(q0 + kConcatChunk, nnz);
-    uint32_t r = __ldg(chunk_row + c), qb = q0;
-    while (qb < q1) {
-      const uint32_t rr = r + lane;
-      const bool ok = rr < rows;
-      const uint32_t s = ok ? __ldg(rp + rr) : 0xFFFFFFFFu;
-      const uint32_t e = ok ? __ldg(rp + rr + 1) : 0xFFFFFFFFu;
-      const uint32_t d = ok ? __ldg(shift + rr) : 0u;
-      const uint32_t lim = min(q1, __shfl_sync(0xffffffffu, e, 31));
-      for (; qb < lim; qb += 32 * U) {
-        uint32_t cv[U];
-        T vv[U];
+  const uint32_t n = *nlong;
+  for (uint32_t x = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < n;
+       x += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t r = long_rows[x];
+    uint32_t o = out_rp[r];
+    for (uint32_t k = 0; k < sa.K; ++k) {
+      const uint32_t s0 = __ldg(sa.rp[k] + r0 + r), e0 = __ldg(sa.rp[k] + r0 + r + 1);
+      const uint32_t off = uint32_t(k * sa.col_stride);
+      const uint32_t* ci = sa.ci[k];
+      const T* val = static_cast<const T*>(sa.val[k]);
+      for (uint32_t tb = s0; tb < e0; tb += 128) {
+        uint32_t cv[4];
+        T vv[4];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t q = qb + 32 * u + lane;
-          if (q < lim) {
-            cv[u] = __ldg(ci + q);
-            vv[u] = __ldg(val + q);
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t t = tb + 32 * u + lane;
+          if (t < e0) {
+            cv[u] = __ldg(ci + t);
+            vv[u] = __ldg(val + t);
           }
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t q = qb + 32 * u + lane;
-          uint32_t j = 0;
-#pragma unroll
-          for (uint32_t step = 16; step >= 1; step >>= 1) {
-            const uint32_t sj = __shfl_sync(0xffffffffu, s, j + step);
-            if (q >= sj) j += step;
-          }
-          const uint32_t dj = __shfl_sync(0xffffffffu, d, j);
-          if (q < lim) {
-            out_ci[dj + q] = cv[u] + off;
-            out_val[dj + q] = vv[u];
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t t = tb + 32 * u + lane;
+          if (t < e0) {
+            out_ci[o + (t - s0)] = cv[u] + off;
+            out_val[o + (t - s0)] = vv[u];
           }
         }
       }
-      qb = lim;
-      r += 32;
+      o += e0 - s0;
     }
   }
 }
@@ -282,13 +279,12 @@ extern "C" int rdmm_spin_delay(uint64_t ns, rdmm_stream_t stream) {
   return RDMM_OK;
 }
 
-extern "C" int rdmm_csr_concat_cols(int dtype_bytes, uint32_t rows, uint32_t K,
-                                    const uint32_t* const* rp,
-                                    const uint32_t* const* ci,
-                                    const void* const* val, const uint64_t* tile_nnz,
-                                    uint64_t col_stride,
-                                    uint32_t* out_rp, uint32_t* out_ci,
-                                    void* out_val, rdmm_stream_t stream) {
+extern "C" int rdmm_csr_concat_cols_rows(int dtype_bytes, uint32_t r0, uint32_t rows,
+                                         uint32_t K, const uint32_t* const* rp,
+                                         const uint32_t* const* ci, const void* const* val,
+                                         uint64_t col_stride, uint32_t* out_rp,
+                                         uint32_t* out_ci, void* out_val,
+                                         rdmm_stream_t stream) {
   if (K == 0 || K > 16) return fail(RDMM_ERR_INVALID, "concat: 1..16 tiles");
   if (col_stride * (K - 1) > 0xFFFFFFFFull)
     return fail(RDMM_ERR_INVALID, "concat: concatenated columns exceed index_t");
@@ -301,45 +297,37 @@ extern "C" int rdmm_csr_concat_cols(int dtype_bytes, uint32_t rows, uint32_t K,
   a.K = K;
   a.col_stride = col_stride;
   cudaStream_t s = as_stream(stream);
-  // chunk table: one entry per kConcatChunk nonzeros of the largest tile
-  uint64_t max_nnz_bound = 0;
-  for (uint32_t k = 0; k < K; ++k) {
-    uint64_t n = 0;
-    if (tile_nnz) {
-      n = tile_nnz[k];
-    } else {
-      uint32_t n32 = 0;
-      RDMM_CUDA_TRY(cudaMemcpyAsync(&n32, rp[k] + rows, 4, cudaMemcpyDeviceToHost, s));
-      RDMM_CUDA_TRY(cudaStreamSynchronize(s));
-      n = n32;
-    }
-    max_nnz_bound = std::max<uint64_t>(max_nnz_bound, n);
-  }
-  const uint32_t cstride = uint32_t(ceil_div(std::max<uint64_t>(max_nnz_bound, 1), kConcatChunk));
-  const size_t shift_bytes = size_t(K) * std::max<uint32_t>(rows, 1) * 4;
-  auto* shift = static_cast<uint32_t*>(scratch(shift_bytes + size_t(K) * cstride * 4, 4, s));
-  if (!shift) return fail(RDMM_ERR_CUDA, "concat: scratch allocation failed");
-  uint32_t* chunk_row = shift + size_t(K) * std::max<uint32_t>(rows, 1);
+  // long-row list: count + up to `rows` entries
+  auto* nlong = static_cast<uint32_t*>(scratch((size_t(rows) + 2) * 4, 4, s));
+  if (!nlong) return fail(RDMM_ERR_CUDA, "concat: scratch allocation failed");
+  RDMM_CUDA_TRY(cudaMemsetAsync(nlong, 0, 4, s));
   const unsigned b1 = unsigned(std::max<uint64_t>(
-      1, std::min<uint64_t>(ceil_div(uint64_t(rows) + 1, 256), uint64_t(num_sms()) * 8)));
-  count_launch(1 + K);
-  k_concat_rows<<<b1, 256, 0, s>>>(a, rows, out_rp, shift, chunk_row, cstride);
-  if (rows) {
-    const unsigned b2 = unsigned(num_sms()) * 8;
-    for (uint32_t k = 0; k < K; ++k) {
-      const uint32_t off = uint32_t(k * col_stride);
-      const uint32_t* sh = shift + uint64_t(k) * rows;
-      const uint32_t* cr = chunk_row + uint64_t(k) * cstride;
-      if (dtype_bytes == 8)
-        k_concat_fill<double><<<b2, 256, 0, s>>>(rp[k], ci[k], static_cast<const double*>(val[k]),
-                                                 rows, off, sh, cr, out_ci,
-                                                 static_cast<double*>(out_val));
-      else
-        k_concat_fill<float><<<b2, 256, 0, s>>>(rp[k], ci[k], static_cast<const float*>(val[k]),
-                                                rows, off, sh, cr, out_ci,
-                                                static_cast<float*>(out_val));
-    }
+      1, std::min<uint64_t>(ceil_div(uint64_t(rows) + 1, 256), uint64_t(num_sms()) * 16)));
+  const unsigned b2 = unsigned(num_sms()) * 8;
+  count_launch(2);
+  if (dtype_bytes == 8) {
+    k_concat_short<double><<<b1, 256, 0, s>>>(a, r0, rows, out_rp, out_ci,
+                                              static_cast<double*>(out_val), nlong + 1, nlong);
+    k_concat_long<double><<<b2, 256, 0, s>>>(a, r0, out_rp, out_ci, static_cast<double*>(out_val),
+                                             nlong + 1, nlong);
+  } else {
+    k_concat_short<float><<<b1, 256, 0, s>>>(a, r0, rows, out_rp, out_ci,
+                                             static_cast<float*>(out_val), nlong + 1, nlong);
+    k_concat_long<float><<<b2, 256, 0, s>>>(a, r0, out_rp, out_ci, static_cast<float*>(out_val),
+                                            nlong + 1, nlong);
   }
   RDMM_CUDA_TRY(cudaGetLastError());
   return RDMM_OK;
+}
+
+extern "C" int rdmm_csr_concat_cols(int dtype_bytes, uint32_t rows, uint32_t K,
+                                    const uint32_t* const* rp,
+                                    const uint32_t* const* ci,
+                                    const void* const* val, const uint64_t* tile_nnz,
+                                    uint64_t col_stride,
+                                    uint32_t* out_rp, uint32_t* out_ci,
+                                    void* out_val, rdmm_stream_t stream) {
+  (void)tile_nnz;
+  return rdmm_csr_concat_cols_rows(dtype_bytes, 0, rows, K, rp, ci, val, col_stride, out_rp,
+                                   out_ci, out_val, stream);
 }
