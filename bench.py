@@ -335,7 +335,9 @@ def run_ours(args, cfg, dev, rank, world):
     ws_base = "stationary_a" if variant == "ws_random" else "stationary_c"
     opts = dict(variant=variant, ws_base=ws_base, checksum=False, record_events=False,
                 fuse_k=not args.no_fuse, lookahead=args.lookahead,
-                split_local=not args.no_split)
+                split_local=not args.no_split, pipeline=not args.no_pipeline,
+                deterministic=args.deterministic,
+                row_blocks=args.row_blocks)
     stream = torch.cuda.ExternalStream(f.stream(rank), device=dev)
 
     def barrier():
@@ -512,7 +514,10 @@ def run_ours(args, cfg, dev, rank, world):
         "config": {"workload": args.config, "desc": cfg["desc"], "permute_seed": args.permute,
                    "rows": m, "cols": k, "n": n,
                    "nnz": nnz_a, "flop_per_step": total_flops,
-                   "variant": variant, "fuse_k": not args.no_fuse, "split_local": not args.no_split, "lookahead": args.lookahead, "grid": f"{pr}x{pc}", "tiles": [tm, tk, tn],
+                   "variant": variant, "fuse_k": not args.no_fuse,
+                   "split_local": not args.no_split, "pipeline": not args.no_pipeline, "deterministic": args.deterministic,
+                   "row_blocks": args.row_blocks or 8, "lookahead": args.lookahead,
+                   "grid": f"{pr}x{pc}", "tiles": [tm, tk, tn],
                    "path": "run_multiply (host C-ABI rdmm_h_run_multiply) over the fabric",
                    "l2": ("inputs > L2 (A %.2f GB, B and C %.2f GB each)"
                           % (nnz_a * 8 / 1e9, m * n * 4 / 1e9)) if cfg["kind"] == "spmm"
@@ -780,6 +785,11 @@ def main():
     ap.add_argument("--no-fuse", action="store_true", help="RunOptions::fuse_k = false")
     ap.add_argument("--no-split", action="store_true", help="RunOptions::split_local = false")
     ap.add_argument("--lookahead", type=int, default=2, help="RunOptions::lookahead")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="RunOptions::deterministic (fused k-order pass per narrow C tile)")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="RunOptions::pipeline = false (whole-tile fetch, then fused pass)")
+    ap.add_argument("--row-blocks", type=int, default=0, help="RunOptions::row_blocks")
     ap.add_argument("--verify", action="store_true",
                     help="check the distributed C against the single-GPU kernel")
     args = ap.parse_args()

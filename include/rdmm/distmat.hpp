@@ -248,11 +248,32 @@ class DistDense {  // distmat.hpp:92-205
   }
 
  private:
-  // Re-initialisation reuses the tile's allocation (same geometry).
+  // Re-initialisation reuses the tile's allocation (same geometry).  B200:
+  // the tiles a rank owns in one tile column are placed back to back in ONE
+  // heap allocation (tile (i,j) right after its owned predecessor in column
+  // j), so a column panel B(:, j) held by one rank is a single row-major
+  // array and the fused SpMM can index it directly instead of by segments.
   GlobalPtr fresh_tile(RankCtx& ctx, std::uint32_t i, std::uint32_t j) {
     const rdmm_gptr old = dir_[geom_.idx(i, j)];
     if (old.length) return GlobalPtr::of(old);
-    return ctx.alloc(std::size_t(geom_.tile_rows(i)) * geom_.tile_cols(j) * sizeof(T));
+    std::uint64_t total = 0;
+    for (std::uint32_t q = 0; q < geom_.M; ++q)
+      if (owner(q, j) == ctx.rank())
+        total += std::uint64_t(geom_.tile_rows(q)) * geom_.tile_cols(j) * sizeof(T);
+    auto pad = [](std::uint64_t b) { return (b + 255) & ~std::uint64_t{255}; };
+    total = 0;
+    for (std::uint32_t q = 0; q < geom_.M; ++q)
+      if (owner(q, j) == ctx.rank())
+        total += pad(std::uint64_t(geom_.tile_rows(q)) * geom_.tile_cols(j) * sizeof(T));
+    GlobalPtr panel = ctx.alloc(total);
+    std::uint64_t off = 0;
+    for (std::uint32_t q = 0; q < geom_.M; ++q) {
+      if (owner(q, j) != ctx.rank()) continue;
+      const std::uint64_t bytes = std::uint64_t(geom_.tile_rows(q)) * geom_.tile_cols(j) * sizeof(T);
+      dir_[geom_.idx(q, j)] = GlobalPtr{panel.rank, panel.offset + off, bytes}.c();
+      off += pad(bytes);
+    }
+    return GlobalPtr::of(dir_[geom_.idx(i, j)]);
   }
   void init_from_any(RankCtx& ctx, const T* global, std::uint64_t ld) {
     for (std::uint32_t i = 0; i < geom_.M; ++i)
@@ -285,10 +306,19 @@ class DistDense {  // distmat.hpp:92-205
 template <typename T>
 class DistSparse {  // distmat.hpp:210-398
  public:
-  struct Entry {  // distmat.hpp:213-216
+  // B200: the tile's entry offsets at the boundaries of kRowBlocks equal row
+  // blocks (row_ptr[b * row_block(rows)], b = 0..kRowBlocks), kept in the
+  // replicated directory so a rank can fetch a remote tile block by block
+  // without first reading its row_ptr (blocks_valid = 0: unknown).
+  static constexpr std::uint32_t kRowBlocks = 16;
+  static std::uint32_t row_block(std::uint32_t rows) { return (rows + kRowBlocks - 1) / kRowBlocks; }
+  struct Entry {  // distmat.hpp:213-216 (+ block offsets)
     rdmm_gptr values, row_ptr, col_idx;
     std::uint64_t nnz = 0;
+    std::uint32_t blocks_valid = 0;
+    std::uint32_t blk_off[kRowBlocks + 1] = {};
   };
+  const Entry& entry(std::uint32_t i, std::uint32_t j) const { return dir_[geom_.idx(i, j)]; }
 
   DistSparse(Fabric& f, std::uint64_t m, std::uint64_t n, std::uint32_t tm, std::uint32_t tn,
              ProcGrid grid, int matrix_id = 0)
@@ -349,6 +379,7 @@ class DistSparse {  // distmat.hpp:210-398
                                      std::uint64_t(j) * geom_.tn, c, rp, &nnz, ctx.stream(0)),
               "extract");
         e.nnz = nnz;
+        set_block_offsets_device(ctx, e, rp, r);
         e.col_idx = ctx.alloc(nnz * sizeof(index_t)).c();
         e.values = ctx.alloc(nnz * sizeof(T)).c();
         check(rdmm_csr_extract_fill(dtype_bytes<T>(), g.row_ptr, g.col_idx, g.values,
@@ -549,9 +580,24 @@ class DistSparse {  // distmat.hpp:210-398
       throw dimension_error("replace_tile: wrong tile dims");
   }
   // distmat.hpp:380-390: 3 allocs + 3 puts
+  void set_block_offsets_device(RankCtx& ctx, Entry& e, const index_t* dev_rp, std::uint32_t rows) {
+    check(rdmm_stream_sync(ctx.stream(0)), "block offsets");
+    const std::uint32_t rb = row_block(rows);
+    for (std::uint32_t b = 0; b <= kRowBlocks; ++b) {
+      const std::uint32_t r = std::min<std::uint64_t>(std::uint64_t(b) * rb, rows);
+      check(rdmm_memcpy(&e.blk_off[b], dev_rp + r, sizeof(index_t), nullptr), "block offsets");
+    }
+    e.blocks_valid = 1;
+  }
   Entry store_host(RankCtx& ctx, const CsrTile<T>& t) {
     Entry e;
     e.nnz = t.nnz();
+    {
+      const std::uint32_t rb = row_block(t.rows);
+      for (std::uint32_t b = 0; b <= kRowBlocks; ++b)
+        e.blk_off[b] = t.row_ptr[std::min<std::uint64_t>(std::uint64_t(b) * rb, t.rows)];
+      e.blocks_valid = 1;
+    }
     e.row_ptr = ctx.alloc(t.row_ptr.size() * sizeof(index_t)).c();
     e.col_idx = ctx.alloc(t.col_idx.size() * sizeof(index_t)).c();
     e.values = ctx.alloc(t.values.size() * sizeof(T)).c();

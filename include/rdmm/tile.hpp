@@ -270,13 +270,14 @@ struct DevDenseTile {
 // (written, never read).  flops == 2*nnz(a)*b.cols.
 template <typename T>
 FlopMeter spmm_local(DevCsrView<T> a, DevDenseConstView<T> b, DevDenseView<T> c,
-                     rdmm_stream_t stream, bool c_zero = false) {
+                     rdmm_stream_t stream, bool c_zero = false, bool atomic = false) {
   if (a.cols != b.rows || c.rows != a.rows || c.cols != b.cols)
     throw dimension_error("spmm_local: dimension mismatch");
   std::uint64_t fl = 0;
   check(rdmm_spmm_csr_ex(dtype_bytes<T>(), a.rows, a.cols, b.cols, a.nnz, a.row_ptr,
                          a.col_idx, a.values, b.values, b.ld, c.values, c.ld,
-                         c_zero ? RDMM_SPMM_C_ZERO : 0u, nullptr, 0, stream, &fl),
+                         (c_zero ? RDMM_SPMM_C_ZERO : 0u) | (atomic ? RDMM_SPMM_ATOMIC : 0u),
+                         nullptr, 0, stream, &fl),
         "spmm_local");
   FlopMeter m;
   m.flops = fl;
@@ -327,6 +328,113 @@ FlopMeter spmm_fused(rdmm_fabric* f, std::uint32_t rank, const std::vector<DevCs
   m.flops = fl;
   m.output_nnz = std::uint64_t(c.rows) * c.cols;
   return m;  // the concat buffers are released stream-ordered after the kernel
+}
+
+// Row-block pipelined form of spmm_fused.  The rows of C are cut at
+// `bounds` (bounds[0] = 0 ... bounds.back() = c.rows); for block b,
+// before_concat(b, side) makes the side stream wait for whatever feeds the
+// block (e.g. the copy-engine slices of remote A tiles), the K-tile
+// concatenation of the block's rows (rdmm_csr_concat_cols_rows) runs on
+// `side` while block b-1 multiplies on `stream`, and the block's SpMM reads
+// its nonzero count on the device (no host round trip).  Two concat buffers
+// alternate.  Same result as spmm_fused (concatenation in the tiles' order).
+//
+// The tiles come in accumulation order (the reference's offset order) with
+// their natural k index `knat`: concatenated column indices are the natural
+// ones (knat[k] * col_stride + c), so when the B tiles form one contiguous
+// panel in natural order (DistDense places a rank's tiles of a column back
+// to back) the SpMM reads B directly, else through the segment table.
+template <typename T, typename BeforeConcat>
+FlopMeter spmm_fused_rows(rdmm_fabric* f, std::uint32_t rank,
+                          const std::vector<DevCsrView<T>>& a,
+                          const std::vector<DevDenseConstView<T>>& b,
+                          const std::vector<std::uint32_t>& knat, std::uint64_t col_stride,
+                          DevDenseView<T> c, rdmm_stream_t stream, rdmm_stream_t side,
+                          bool c_zero, const std::vector<std::uint32_t>& bounds,
+                          BeforeConcat&& before_concat) {
+  const std::size_t K = a.size();
+  if (K == 0 || b.size() != K || K > 16) throw std::invalid_argument("spmm_fused_rows: 1..16 tiles");
+  if (bounds.size() < 2 || bounds.front() != 0 || bounds.back() != c.rows)
+    throw std::invalid_argument("spmm_fused_rows: bad row bounds");
+  std::uint64_t nnz = 0;
+  std::vector<const index_t*> rp(K), ci(K);
+  std::vector<const void*> vv(K), bs(K, nullptr);
+  std::vector<std::uint64_t> coff(K);
+  if (knat.size() != K) throw std::invalid_argument("spmm_fused_rows: knat size");
+  for (std::size_t k = 0; k < K; ++k) {
+    if (a[k].rows != c.rows || a[k].cols != b[k].rows || b[k].cols != c.cols ||
+        b[k].ld != b[0].ld || b[k].rows > col_stride || knat[k] >= K || bs[knat[k]])
+      throw dimension_error("spmm_fused_rows: dimension mismatch");
+    nnz += a[k].nnz;
+    rp[k] = a[k].row_ptr;
+    ci[k] = a[k].col_idx;
+    vv[k] = a[k].values;
+    bs[knat[k]] = b[k].values;
+    coff[k] = std::uint64_t(knat[k]) * col_stride;
+  }
+  // one contiguous B panel in natural order?
+  bool panel = true;
+  for (std::size_t k = 1; k < K; ++k)
+    panel &= static_cast<const T*>(bs[k]) ==
+             static_cast<const T*>(bs[0]) + std::uint64_t(k) * col_stride * b[0].ld;
+  FlopMeter m;
+  m.flops = 2ull * nnz * c.cols;
+  m.output_nnz = std::uint64_t(c.rows) * c.cols;
+  const std::size_t blocks = bounds.size() - 1;
+  std::uint32_t rbmax = 0;
+  for (std::size_t q = 0; q < blocks; ++q) rbmax = std::max(rbmax, bounds[q + 1] - bounds[q]);
+  DevBuffer rpb[2], cib[2], vvb[2];
+  const std::size_t nbuf = blocks > 1 ? 2 : 1;
+  for (std::size_t q = 0; q < nbuf; ++q) {
+    rpb[q] = DevBuffer(f, rank, (std::uint64_t(rbmax) + 1) * sizeof(index_t), stream);
+    cib[q] = DevBuffer(f, rank, std::max<std::uint64_t>(nnz, 1) * sizeof(index_t), stream);
+    vvb[q] = DevBuffer(f, rank, std::max<std::uint64_t>(nnz, 1) * sizeof(T), stream);
+  }
+  // the side stream starts after the buffers exist (allocated on `stream`)
+  void* ready = nullptr;
+  check(rdmm_event_record(stream, &ready), "spmm_fused_rows");
+  check(rdmm_event_wait(ready, side), "spmm_fused_rows");
+  rdmm_event_destroy(ready);
+  std::vector<void*> spmm_done(blocks, nullptr);
+  for (std::size_t bk = 0; bk < blocks; ++bk) {
+    const std::size_t q = bk % nbuf;
+    const std::uint32_t r0 = bounds[bk], nr = bounds[bk + 1] - bounds[bk];
+    before_concat(bk, side);
+    if (nr == 0) continue;
+    if (bk >= nbuf && spmm_done[bk - nbuf])
+      check(rdmm_event_wait(spmm_done[bk - nbuf], side), "spmm_fused_rows");
+    check(rdmm_csr_concat_cols_rows(dtype_bytes<T>(), r0, nr, std::uint32_t(K), rp.data(),
+                                    ci.data(), vv.data(), col_stride, coff.data(),
+                                    static_cast<index_t*>(rpb[q].get()),
+                                    static_cast<index_t*>(cib[q].get()), vvb[q].get(), side),
+          "spmm_fused_rows concat");
+    void* cat = nullptr;
+    check(rdmm_event_record(side, &cat), "spmm_fused_rows");
+    check(rdmm_event_wait(cat, stream), "spmm_fused_rows");
+    rdmm_event_destroy(cat);
+    std::uint64_t fl = 0;
+    const unsigned flags = (c_zero ? RDMM_SPMM_C_ZERO : 0u) | RDMM_SPMM_NNZ_ON_DEVICE;
+    if (panel)
+      check(rdmm_spmm_csr_ex(dtype_bytes<T>(), nr, std::uint32_t(col_stride * K), c.cols,
+                             std::max<std::uint64_t>(nnz, 1),
+                             static_cast<const index_t*>(rpb[q].get()),
+                             static_cast<const index_t*>(cib[q].get()), vvb[q].get(), bs[0],
+                             b[0].ld, c.values + std::uint64_t(r0) * c.ld, c.ld, flags, nullptr, 0,
+                             stream, &fl),
+            "spmm_fused_rows");
+    else
+      check(rdmm_spmm_csr_seg(dtype_bytes<T>(), nr, c.cols, std::max<std::uint64_t>(nnz, 1),
+                              static_cast<const index_t*>(rpb[q].get()),
+                              static_cast<const index_t*>(cib[q].get()), vvb[q].get(), bs.data(),
+                              std::uint32_t(K), std::uint32_t(col_stride), b[0].ld,
+                              c.values + std::uint64_t(r0) * c.ld, c.ld, flags, nullptr, 0, stream,
+                              &fl),
+            "spmm_fused_rows");
+    check(rdmm_event_record(stream, &spmm_done[bk]), "spmm_fused_rows");
+  }
+  for (void* e : spmm_done)
+    if (e) rdmm_event_destroy(e);
+  return m;  // the buffers are released stream-ordered after the last SpMM
 }
 
 // c += x (tile.hpp:300-307); x may live in a peer GPU's heap (NVLink loads).

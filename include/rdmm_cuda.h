@@ -94,6 +94,19 @@ int rdmm_spmm_csr_f64(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
  *                         identical to the accumulate form on a zero C.
  */
 #define RDMM_SPMM_C_ZERO 1u
+/*   RDMM_SPMM_NNZ_ON_DEVICE  nnz is only an upper bound: the kernels read the
+ *                         real count from row_ptr[rows] on the device (a CSR
+ *                         produced by an earlier kernel on the same stream,
+ *                         e.g. a row block of rdmm_csr_concat_cols_rows);
+ *                         flops is reported as 0. */
+#define RDMM_SPMM_NNZ_ON_DEVICE 2u
+/*   RDMM_SPMM_ATOMIC     accumulate into C with red.global.add (rows of at most
+ *                         31 vectors, the narrow slot kernels; ignored
+ *                         otherwise): C is never read, several products into
+ *                         the same C may run concurrently; the summation
+ *                         order of a row varies between runs (exact for
+ *                         integer data, within the fp tolerance otherwise). */
+#define RDMM_SPMM_ATOMIC 4u
 int rdmm_spmm_csr_ex(int dtype_bytes, uint32_t rows, uint32_t cols, uint32_t n,
                      uint64_t nnz, const uint32_t* row_ptr,
                      const uint32_t* col_idx, const void* val, const void* B,
@@ -195,12 +208,14 @@ int rdmm_csr_concat_cols(int dtype_bytes, uint32_t rows, uint32_t K,
                          void* out_val, rdmm_stream_t stream);
 /* The same for the block of rows [r0, r0+rows) of the tiles: a standalone
  * CSR (out_rp[0] = 0) of those rows, e.g. one row block of a pipelined
- * fused stationary-C step. */
+ * fused stationary-C step.  col_offsets (host, K entries; NULL = k *
+ * col_stride) sets the column offset of each tile, e.g. its natural column
+ * position when the tiles are concatenated in a rotated order. */
 int rdmm_csr_concat_cols_rows(int dtype_bytes, uint32_t r0, uint32_t rows, uint32_t K,
                               const uint32_t* const* row_ptr, const uint32_t* const* col_idx,
                               const void* const* values, uint64_t col_stride,
-                              uint32_t* out_rp, uint32_t* out_ci, void* out_val,
-                              rdmm_stream_t stream);
+                              const uint64_t* col_offsets, uint32_t* out_rp, uint32_t* out_ci,
+                              void* out_val, rdmm_stream_t stream);
 /* Sum of a dense tile's values in double (checksum, algos.hpp:634-669). */
 int rdmm_tile_sum(int dtype_bytes, uint32_t rows, uint32_t cols, uint64_t ld,
                   const void* p, rdmm_stream_t stream, double* out);
@@ -297,7 +312,8 @@ uint32_t rdmm_fabric_node_group(const rdmm_fabric* f);
 uint64_t rdmm_fabric_queue_capacity(const rdmm_fabric* f);
 int rdmm_fabric_is_local(const rdmm_fabric* f, uint32_t rank);
 int rdmm_fabric_device(const rdmm_fabric* f, uint32_t rank); /* local only */
-/* Per-local-rank streams owned by the fabric: 0 = compute, 1..2 = copy. */
+/* Per-local-rank streams owned by the fabric: 0 = compute, 1..2 = copy,
+ * 3 = side compute (work overlapped with stream 0, e.g. a pipelined concat). */
 rdmm_stream_t rdmm_fabric_stream(rdmm_fabric* f, uint32_t rank, int which);
 /* Process-local sequence number (1, 2, ...): processes that create objects
  * in the same order get the same numbers (collective tags). */

@@ -85,6 +85,9 @@ typedef struct {
   int fuse_k;
   int split_local; /* fused stationary-C: local products first on the first tile */
   int time_stages; /* per-k-step device time of each rank's multiplies (stage_ms) */
+  int pipeline;    /* narrow fused stationary-C: row-block fetch/concat/SpMM pipeline */
+  int row_blocks;  /* row blocks of that pipeline (0 = default) */
+  int deterministic; /* reproducible k-order accumulation of narrow dense C tiles */
 } rdmm_h_options;
 
 #define RDMM_H_MAX_RANKS 64

@@ -162,7 +162,8 @@ struct Local {
   uint32_t rank = 0;
   int device = 0;
   Heap heap;
-  cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+  // 0 compute, 1-2 copy engines, 3 side compute (concat of pipelined fetches)
+  cudaStream_t streams[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t label = 0;
   bool sink = false;
   std::vector<rdmm_event> events;
@@ -564,7 +565,7 @@ extern "C" int rdmm_fabric_device(const rdmm_fabric* f, uint32_t rank) {
 extern "C" rdmm_stream_t rdmm_fabric_stream(rdmm_fabric* f, uint32_t rank,
                                             int which) {
   Local* L = f->local(rank);
-  if (!L || which < 0 || which > 2) return nullptr;
+  if (!L || which < 0 || which > 3) return nullptr;
   return reinterpret_cast<rdmm_stream_t>(L->streams[which]);
 }
 extern "C" uint64_t rdmm_fabric_next_uid(rdmm_fabric* f) { return ++f->uid; }

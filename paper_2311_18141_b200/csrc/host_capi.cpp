@@ -101,6 +101,9 @@ RunOptions opts_of(const rdmm_h_options* o) {
   r.fuse_k = o->fuse_k != 0;
   r.split_local = o->split_local != 0;
   r.time_stages = o->time_stages != 0;
+  r.pipeline = o->pipeline != 0;
+  if (o->row_blocks > 0) r.row_blocks = std::uint32_t(o->row_blocks);
+  r.deterministic = o->deterministic != 0;
   return r;
 }
 

@@ -18,6 +18,7 @@
 //  * col_idx/val are read 32 at a time (one coalesced load per lane) and
 //    broadcast with shuffles.
 #include <algorithm>
+#include <atomic>
 
 #include <cstdlib>
 #include <string>
@@ -140,6 +141,13 @@ struct SpmmArgs {
   T* __restrict__ tail_val;  // [nchunks][wstride]
   int32_t* __restrict__ tail_row;  // [nchunks]
   const uint32_t* __restrict__ chunk_row;  // [nchunks] row holding nonzero c*Q
+  // RDMM_SPMM_NNZ_ON_DEVICE: nnz = *dyn_end (= rp[rows]) read by the kernels,
+  // nchunks an upper bound and Q derived on the device (no host round trip)
+  const uint32_t* __restrict__ dyn_end;
+  // RDMM_SPMM_ATOMIC (narrow slot kernels): every row flush, including the
+  // pieces of rows cut by chunk boundaries, is a red.global.add into C; no
+  // C read, no head/tail fix-up, products of several launches may overlap
+  int atomic;
   uint64_t ldb, ldc;
   uint64_t nnz, Q;
   uint32_t rows, nvec, nchunks, wstride;
@@ -198,6 +206,7 @@ __device__ __forceinline__ unsigned group_mask() {
 }
 
 constexpr int kThreads = 256;
+constexpr int kMaxDevices = 64;
 constexpr int kWin = 32;  // nonzeros staged per window
 constexpr int kU = 8;     // B-row gathers in flight per worker
 
@@ -390,11 +399,33 @@ __global__ void __launch_bounds__(kThreads, MINB)
 }
 
 
+// Chunking of a launch: nnz, chunk length Q and chunk count, from the host
+// plan or, with a device-resident nnz, derived on the device from the
+// planned chunk count (an upper bound).
+struct Chunking {
+  uint32_t nnz, Q, nch;
+};
+__device__ __forceinline__ Chunking chunking(uint64_t nnz, uint64_t Q, uint32_t nchunks,
+                                             const uint32_t* dyn_end) {
+  if (!dyn_end) return {uint32_t(nnz), uint32_t(Q), nchunks};
+  // at least 256 nonzeros per chunk: a small block gets fewer, longer chunks
+  const uint32_t n = __ldg(dyn_end);
+  const uint32_t q = max(256u, (n + nchunks - 1) / nchunks);
+  return {n, q, n ? (n + q - 1) / q : 0u};
+}
+template <typename T>
+__device__ __forceinline__ Chunking chunking(const SpmmArgs<T>& p) {
+  return chunking(p.nnz, p.Q, p.nchunks, p.dyn_end);
+}
+
 // Chunk start rows: chunk c begins at nonzero c*Q, inside the row r with
 // rp[r] <= c*Q < rp[r+1].  One coalesced pass over the row pointer replaces
 // a 22-step dependent binary search per chunk in the SpMM kernels.
-__global__ void spmm_chunk_rows(const uint32_t* __restrict__ rp, uint32_t rows, uint64_t Q,
-                                uint32_t nchunks, uint32_t* __restrict__ chunk_row) {
+__global__ void spmm_chunk_rows(const uint32_t* __restrict__ rp, uint32_t rows, uint64_t Q0,
+                                uint32_t nchunks, uint32_t* __restrict__ chunk_row,
+                                const uint32_t* __restrict__ dyn_end) {
+  const Chunking ck = chunking(0, Q0, nchunks, dyn_end);
+  const uint64_t Q = dyn_end ? ck.Q : Q0;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows;
        r += gridDim.x * blockDim.x) {
     const uint64_t s = __ldg(rp + r), e = __ldg(rp + r + 1);
@@ -481,13 +512,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
   const uint32_t col0 = v * VEC + coff;  // first owned column within the row
   constexpr unsigned full = 0xffffffffu;
   // positions fit in 32 bits: row_ptr is uint32 (tile.hpp:17)
-  const uint32_t nnz = uint32_t(p.nnz), Q = uint32_t(p.Q);
+  const Chunking ck = chunking(p);
+  const uint32_t nnz = ck.nnz, Q = ck.Q, nch = ck.nch;
   auto chunk_hi = [&](uint32_t c) { return uint32_t(umin(uint64_t(c) * Q + Q, nnz)); };
 
   // issue side of the ring: windows of the warp's chunks in consume order
   uint32_t ic = warp, iw = warp * Q, ist = 0;
   auto issue = [&]() {
-    if (ic < p.nchunks) {
+    if (ic < nch) {
       const uint32_t h = chunk_hi(ic);
 #pragma unroll
       for (int j = 0; j < SLW; ++j) {
@@ -542,7 +574,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
   auto cload = [&](uint32_t row, bool starts, T (&cin)[LEN]) {
 #pragma unroll
     for (int x = 0; x < LEN; ++x)
-      cin[x] = (!CZERO && starts && owner) ? __ldcs(Cs + uint64_t(row) * p.ldc + col0 + x) : T(0);
+      cin[x] = (!CZERO && !p.atomic && starts && owner)
+                   ? __ldcs(Cs + uint64_t(row) * p.ldc + col0 + x)
+                   : T(0);
   };
   auto put = [&](T* dst, const T (&o)[LEN]) {
 #pragma unroll
@@ -554,14 +588,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
   };
 
   uint32_t cst = 0;  // consume-side ring stage
-  uint32_t nrow = warp < p.nchunks ? __ldg(p.chunk_row + warp) : 0;
-  for (uint32_t c = warp; c < p.nchunks; c += nwarps) {
+  uint32_t nrow = warp < nch ? __ldg(p.chunk_row + warp) : 0;
+  for (uint32_t c = warp; c < nch; c += nwarps) {
     const uint32_t lo = c * Q, hi = chunk_hi(c);
     uint32_t row = nrow, rb = row;
     uint32_t rew[1];
     win_load<32, 1>(rew, p.rp, rb, p.rows, lane);
     bool starts = __ldg(p.rp + row) >= lo;
-    if (c + nwarps < p.nchunks) nrow = __ldg(p.chunk_row + c + nwarps);
+    if (c + nwarps < nch) nrow = __ldg(p.chunk_row + c + nwarps);
     uint32_t rend = win_get<32, 1>(rew, 0, full);
     uint32_t rstart = lo;
     V acc = vzero<V>();
@@ -572,7 +606,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
       T o[LEN];
       reduce(acc, o);
       if (owner) {
-        if (starts) {
+        if (p.atomic) {
+#pragma unroll
+          for (int x = 0; x < LEN; ++x) atomicAdd(Cs + uint64_t(row) * p.ldc + col0 + x, o[x]);
+        } else if (starts) {
           if (!CZERO)
 #pragma unroll
             for (int x = 0; x < LEN; ++x) o[x] = cin[x] + o[x];
@@ -658,7 +695,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll
       for (int x = 0; x < LEN; ++x) o[x] = cin[x] + o[x];
     int32_t trow = -1;
-    if (rend <= hi && starts) {
+    if (p.atomic) {
+      if (owner)
+#pragma unroll
+        for (int x = 0; x < LEN; ++x) atomicAdd(Cs + uint64_t(row) * p.ldc + col0 + x, o[x]);
+    } else if (rend <= hi && starts) {
       if (owner) put_cs(Cs + uint64_t(row) * p.ldc + col0, o);
     } else {
       if (owner) put((starts ? p.tail_val : p.head_val) + uint64_t(c) * p.wstride + col0, o);
@@ -750,7 +791,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t col0 = v * VEC + coff;
   constexpr unsigned full = 0xffffffffu;
   // positions fit in 32 bits: row_ptr is uint32 (tile.hpp:17)
-  const uint32_t nnz = uint32_t(p.nnz), Q = uint32_t(p.Q), nch = p.nchunks;
+  const Chunking ck = chunking(p);
+  const uint32_t nnz = ck.nnz, Q = ck.Q, nch = ck.nch;
   auto chunk_hi = [&](uint32_t lo) { return nnz - lo > Q ? lo + Q : nnz; };
 
   // issue sides: (chunk, window start, chunk end) of the next col/val window
@@ -863,13 +905,17 @@ __global__ void __launch_bounds__(kThreads, 2)
     T cin[LEN];
     T* crow = Cs + uint64_t(row) * p.ldc + col0;
 #pragma unroll
-    for (int x = 0; x < LEN; ++x) cin[x] = (!CZERO && starts && owner) ? __ldcs(crow + x) : T(0);
+    for (int x = 0; x < LEN; ++x)
+      cin[x] = (!CZERO && !p.atomic && starts && owner) ? __ldcs(crow + x) : T(0);
     // flush the current row (it ends at rend) and move to the next one
     auto flush = [&]() {
       T o[LEN];
       reduce(acc, o);
       if (owner) {
-        if (starts) {
+        if (p.atomic) {
+#pragma unroll
+          for (int x = 0; x < LEN; ++x) atomicAdd(crow + x, o[x]);
+        } else if (starts) {
 #pragma unroll
           for (int x = 0; x < LEN; ++x) __stcs(crow + x, CZERO ? o[x] : cin[x] + o[x]);
         } else {
@@ -892,7 +938,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       acc = vzero<V>();
       crow = Cs + uint64_t(row) * p.ldc + col0;
 #pragma unroll
-      for (int x = 0; x < LEN; ++x) cin[x] = (!CZERO && owner) ? __ldcs(crow + x) : T(0);
+      for (int x = 0; x < LEN; ++x) cin[x] = (!CZERO && !p.atomic && owner) ? __ldcs(crow + x) : T(0);
     };
     for (uint32_t w = lo; w < hi; w += 32) {
       issue_a();
@@ -952,7 +998,11 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
       for (int x = 0; x < LEN; ++x) o[x] = cin[x] + o[x];
     int32_t trow = -1;
-    if (rend <= hi && starts) {
+    if (p.atomic) {
+      if (owner)
+#pragma unroll
+        for (int x = 0; x < LEN; ++x) atomicAdd(crow + x, o[x]);
+    } else if (rend <= hi && starts) {
       if (owner)
 #pragma unroll
         for (int x = 0; x < LEN; ++x) __stcs(crow + x, o[x]);
@@ -1166,7 +1216,8 @@ __global__ void __launch_bounds__(kThreads) spmm_fixup(const SpmmArgs<T> p) {
   V* __restrict__ Cv = reinterpret_cast<V*>(p.C);
   const V* hv = reinterpret_cast<const V*>(p.head_val);
   const V* tv = reinterpret_cast<const V*>(p.tail_val);
-  for (uint32_t c = worker; c < p.nchunks; c += nworkers) {
+  const Chunking ck = chunking(p);
+  for (uint32_t c = worker; c < ck.nch; c += nworkers) {
     const int32_t r = p.tail_row[c];
     if (r < 0) continue;
     const uint64_t re = p.rp[r + 1];
@@ -1174,12 +1225,12 @@ __global__ void __launch_bounds__(kThreads) spmm_fixup(const SpmmArgs<T> p) {
 #pragma unroll
     for (int v = 0; v < NV; ++v)
       if (lane + G * v < p.nvec) acc[v] = tv[uint64_t(c) * ws + lane + G * v];
-    for (uint32_t c2 = c + 1; c2 < p.nchunks; ++c2) {
+    for (uint32_t c2 = c + 1; c2 < ck.nch; ++c2) {
 #pragma unroll
       for (int v = 0; v < NV; ++v)
         if (lane + G * v < p.nvec)
           acc[v] = vadd(acc[v], hv[uint64_t(c2) * ws + lane + G * v]);
-      if (re <= umin(uint64_t(c2 + 1) * p.Q, p.nnz)) break;
+      if (re <= umin(uint64_t(c2 + 1) * ck.Q, ck.nnz)) break;
     }
 #pragma unroll
     for (int v = 0; v < NV; ++v)
@@ -1230,14 +1281,18 @@ void launch_seg(const SpmmArgs<T>& a, bool czero, int blocks, cudaStream_t s) {
     } else if (kv == 0 && G <= 8 && VEC * sizeof(T) == 16 && async_mode()) {
       const size_t sm = AsyncCfg<T>::smem(G);
       auto fn = czero ? spmm_slots_async<T, S, true, SEG> : spmm_slots_async<T, S, false, SEG>;
-      static int resident[2] = {0, 0};  // CTAs per SM (persistent grid)
-      if (!resident[czero]) {
+      // the dynamic shared-memory opt-in is per device
+      static std::atomic<int> resident[2][kMaxDevices] = {};  // CTAs per SM (persistent grid)
+      int dev = 0;
+      cudaGetDevice(&dev);
+      std::atomic<int>& res = resident[czero][dev < kMaxDevices ? dev : 0];
+      if (!res.load()) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         int nb = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, sm);
-        resident[czero] = nb > 0 ? nb : 1;
+        res.store(nb > 0 ? nb : 1);
       }
-      fn<<<std::min(blocks, resident[czero] * num_sms()), kThreads, sm, s>>>(a);
+      fn<<<std::min(blocks, res.load() * num_sms()), kThreads, sm, s>>>(a);
     } else if (kv == 1) {
       if (czero) spmm_rows<T, VEC, G, NV, true, 1, SEG><<<blocks, kThreads, 0, s>>>(a);
       else spmm_rows<T, VEC, G, NV, false, 1, SEG><<<blocks, kThreads, 0, s>>>(a);
@@ -1268,7 +1323,7 @@ void launch(const SpmmArgs<T>& a, bool czero, int blocks, int fix_blocks,
     launch_seg<T, VEC, G, NV, true>(a, czero, blocks, s);
   else
     launch_seg<T, VEC, G, NV, false>(a, czero, blocks, s);
-  spmm_fixup<T, VEC, G, NV><<<fix_blocks, kThreads, 0, s>>>(a);
+  if (!a.atomic) spmm_fixup<T, VEC, G, NV><<<fix_blocks, kThreads, 0, s>>>(a);
 }
 
 template <typename T, int VEC>
@@ -1389,7 +1444,8 @@ int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
               uint64_t ldb, T* C, uint64_t ldc, unsigned flags, void* ws,
               size_t ws_bytes, rdmm_stream_t stream, uint64_t* flops,
               const T* const* bseg = nullptr, uint32_t nseg = 0, uint32_t seg_rows = 0) {
-  if (flops) *flops = 2ull * nnz * n;
+  bool dyn = (flags & RDMM_SPMM_NNZ_ON_DEVICE) != 0;
+  if (flops) *flops = dyn ? 0 : 2ull * nnz * n;
   const bool czero = (flags & RDMM_SPMM_C_ZERO) != 0;
   if (ldb < n || ldc < n)
     return fail(RDMM_ERR_DIMENSION, "spmm: leading dimension smaller than n");
@@ -1414,7 +1470,20 @@ int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
   const bool v32_ok = !async_rows && v32_mode() != 0 && kernel_variant() == 0 && n % (2 * VV) == 0 &&
                       ldb % (2 * VV) == 0 && ldc % (2 * VV) == 0 && aligned(32) &&
                       uint64_t(n) * sizeof(T) <= max_row;
-  const SpmmPlan P = make_plan<T>(rows, nnz, n, v32_ok ? 2 : vec_ok ? 1 : 0);
+  const int vmode = v32_ok ? 2 : vec_ok ? 1 : 0;
+  const uint32_t vec_chosen = vmode == 2 ? 2 * VV : vmode == 1 ? VV : 1;
+  // the narrow slot kernels chunk on the device; the others need nnz here
+  const bool narrow_slots = kernel_variant() == 0 && n / vec_chosen < 32;
+  if (dyn && !narrow_slots) {
+    // only the narrow cp.async kernel chunks on the device: read nnz here
+    uint32_t nd = 0;
+    RDMM_CUDA_TRY(cudaMemcpyAsync(&nd, rp + rows, 4, cudaMemcpyDeviceToHost, s));
+    RDMM_CUDA_TRY(cudaStreamSynchronize(s));
+    nnz = nd;
+    dyn = false;
+    if (nnz == 0) return RDMM_OK;
+  }
+  const SpmmPlan P = make_plan<T>(rows, nnz, n, vmode);
   void* w = ws;
   if (!w || ws_bytes < P.bytes) {
     if (ws) return fail(RDMM_ERR_INVALID, "spmm: workspace too small");
@@ -1447,10 +1516,14 @@ int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
   a.tail_row = reinterpret_cast<int32_t*>(base + 2 * vbytes);
   uint32_t* chunk_row = reinterpret_cast<uint32_t*>(base + 2 * vbytes + size_t(P.nchunks) * 4);
   a.chunk_row = chunk_row;
+  a.dyn_end = dyn ? rp + rows : nullptr;
+  // atomic accumulation: the narrow slot kernels only (others ignore it)
+  a.atomic = (flags & RDMM_SPMM_ATOMIC) != 0 && narrow_slots;
   const uint32_t nvec_total = n / P.VEC;
   KernelTimer timer(s, 1);
   count_launch(1);
-  spmm_chunk_rows<<<P.chunk_blocks, kThreads, 0, s>>>(rp, rows, P.Q, P.nchunks, chunk_row);
+  spmm_chunk_rows<<<P.chunk_blocks, kThreads, 0, s>>>(rp, rows, P.Q, P.nchunks, chunk_row,
+                                                      a.dyn_end);
   for (uint32_t v0 = 0; v0 < nvec_total; v0 += P.pv) {
     count_launch(2);
     const uint32_t nv = std::min<uint32_t>(P.pv, nvec_total - v0);

@@ -78,8 +78,8 @@ struct ConcatArgs {
   const uint32_t* rp[16];
   const uint32_t* ci[16];
   const void* val[16];
+  uint32_t off[16];  // column offset added to tile k's indices
   uint32_t K;
-  uint64_t col_stride;
 };
 
 // The tile pointer tables are staged in shared memory: indexing the
@@ -89,10 +89,10 @@ __device__ __forceinline__ void stage_args(const ConcatArgs& a, ConcatArgs& sa) 
     sa.rp[threadIdx.x] = a.rp[threadIdx.x];
     sa.ci[threadIdx.x] = a.ci[threadIdx.x];
     sa.val[threadIdx.x] = a.val[threadIdx.x];
+    sa.off[threadIdx.x] = a.off[threadIdx.x];
   }
   if (threadIdx.x == 0) {
     sa.K = a.K;
-    sa.col_stride = a.col_stride;
   }
   __syncthreads();
 }
@@ -133,13 +133,26 @@ __global__ void k_concat_short(ConcatArgs a, uint32_t r0, uint32_t rows,
     }
     for (uint32_t k = 0; k < K; ++k) {
       const uint32_t s0 = __ldg(sa.rp[k] + r0 + r), e0 = __ldg(sa.rp[k] + r0 + r + 1);
-      const uint32_t off = uint32_t(k * sa.col_stride);
+      const uint32_t off = sa.off[k];
       const uint32_t* ci = sa.ci[k];
       const T* val = static_cast<const T*>(sa.val[k]);
-      for (uint32_t t = s0; t < e0; ++t, ++o) {
-        out_ci[o] = __ldg(ci + t) + off;
-        out_val[o] = __ldg(val + t);
+      for (uint32_t t = s0; t < e0; t += 4, o += 4) {
+        uint32_t cv[4];
+        T vv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (t + u < e0) {
+            cv[u] = __ldg(ci + t + u);
+            vv[u] = __ldg(val + t + u);
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (t + u < e0) {
+            out_ci[o + u] = cv[u] + off;
+            out_val[o + u] = vv[u];
+          }
       }
+      o -= (4 - (e0 - s0) % 4) % 4;
     }
   }
 }
@@ -159,7 +172,7 @@ __global__ void k_concat_long(ConcatArgs a, uint32_t r0, const uint32_t* __restr
     uint32_t o = out_rp[r];
     for (uint32_t k = 0; k < sa.K; ++k) {
       const uint32_t s0 = __ldg(sa.rp[k] + r0 + r), e0 = __ldg(sa.rp[k] + r0 + r + 1);
-      const uint32_t off = uint32_t(k * sa.col_stride);
+      const uint32_t off = sa.off[k];
       const uint32_t* ci = sa.ci[k];
       const T* val = static_cast<const T*>(sa.val[k]);
       for (uint32_t tb = s0; tb < e0; tb += 128) {
@@ -282,20 +295,21 @@ extern "C" int rdmm_spin_delay(uint64_t ns, rdmm_stream_t stream) {
 extern "C" int rdmm_csr_concat_cols_rows(int dtype_bytes, uint32_t r0, uint32_t rows,
                                          uint32_t K, const uint32_t* const* rp,
                                          const uint32_t* const* ci, const void* const* val,
-                                         uint64_t col_stride, uint32_t* out_rp,
-                                         uint32_t* out_ci, void* out_val,
+                                         uint64_t col_stride, const uint64_t* col_offsets,
+                                         uint32_t* out_rp, uint32_t* out_ci, void* out_val,
                                          rdmm_stream_t stream) {
   if (K == 0 || K > 16) return fail(RDMM_ERR_INVALID, "concat: 1..16 tiles");
-  if (col_stride * (K - 1) > 0xFFFFFFFFull)
-    return fail(RDMM_ERR_INVALID, "concat: concatenated columns exceed index_t");
   ConcatArgs a{};
   for (uint32_t k = 0; k < K; ++k) {
     a.rp[k] = rp[k];
     a.ci[k] = ci[k];
     a.val[k] = val[k];
+    const uint64_t off = col_offsets ? col_offsets[k] : uint64_t(k) * col_stride;
+    if (off > 0xFFFFFFFFull)
+      return fail(RDMM_ERR_INVALID, "concat: concatenated columns exceed index_t");
+    a.off[k] = uint32_t(off);
   }
   a.K = K;
-  a.col_stride = col_stride;
   cudaStream_t s = as_stream(stream);
   // long-row list: count + up to `rows` entries
   auto* nlong = static_cast<uint32_t*>(scratch((size_t(rows) + 2) * 4, 4, s));
@@ -328,6 +342,6 @@ extern "C" int rdmm_csr_concat_cols(int dtype_bytes, uint32_t rows, uint32_t K,
                                     uint32_t* out_rp, uint32_t* out_ci,
                                     void* out_val, rdmm_stream_t stream) {
   (void)tile_nnz;
-  return rdmm_csr_concat_cols_rows(dtype_bytes, 0, rows, K, rp, ci, val, col_stride, out_rp,
-                                   out_ci, out_val, stream);
+  return rdmm_csr_concat_cols_rows(dtype_bytes, 0, rows, K, rp, ci, val, col_stride, nullptr,
+                                   out_rp, out_ci, out_val, stream);
 }

@@ -26,7 +26,8 @@ class Options(C.Structure):
                 ("random_delay_ms_max", C.c_double), ("record_events", C.c_int),
                 ("record_triples", C.c_int), ("lookahead", C.c_int),
                 ("ws_local_inplace", C.c_int), ("checksum", C.c_int), ("fuse_k", C.c_int),
-                ("split_local", C.c_int), ("time_stages", C.c_int)]
+                ("split_local", C.c_int), ("time_stages", C.c_int), ("pipeline", C.c_int),
+                ("row_blocks", C.c_int), ("deterministic", C.c_int)]
 
 
 class Report(C.Structure):
@@ -321,12 +322,14 @@ def run_multiply(f: Fabric, A: DistSparse, B, Cm, variant="stationary_c", ws_bas
                  prefetch=True, offset=True, seed=0, delay_ns_per_flop=0.0,
                  random_delay_ms_max=0.0, record_events=True, record_triples=False,
                  lookahead=2, ws_local_inplace=True, checksum=True, fuse_k=True,
-                 split_local=True, time_stages=False) -> RunReport:
+                 split_local=True, time_stages=False, pipeline=True, row_blocks=0,
+                 deterministic=False) -> RunReport:
     """C += A*B on the fabric -- algos.hpp:673-752."""
     o = Options(VARIANTS.index(variant), VARIANTS.index(ws_base), int(prefetch), int(offset),
                 seed, delay_ns_per_flop, random_delay_ms_max, int(record_events),
                 int(record_triples), lookahead, int(ws_local_inplace), int(checksum),
-                int(fuse_k), int(split_local), int(time_stages))
+                int(fuse_k), int(split_local), int(time_stages), int(pipeline), int(row_blocks),
+                int(deterministic))
     r = Report()
     L.check(_h.rdmm_h_run_multiply(f._h, A._h, B._h, Cm._h, C.byref(o), C.byref(r)),
             "run_multiply")
