@@ -456,43 +456,74 @@ def run_ours(args, cfg, dev, rank, world):
             "algorithmic_bytes": alg, "peak_source": peak_src, "kernel": kernel,
             "kernel_ms_per_step": kms_step, "kernel_launches_timed": kcount}
 
-    # ---- e2e: the same step through the public API from pinned host buffers
+    # ---- e2e: the same step through the public API from pinned HOST buffers.
+    # Every step uploads its inputs (A's CSR arrays and B, pinned host ->
+    # device staging on its own stream), builds the distributed operands from
+    # them (init_from_device: A's tiles cut, B's tiles scattered on the
+    # device), multiplies (run_multiply), and downloads its C tiles
+    # (owned_to_host_async on a second stream).  Steps are pipelined the way a
+    # serving loop would run them: step s+1's upload (H2D copy engine) and
+    # step s's download (D2H copy engine) overlap, with two staging buffers
+    # and two C matrices alternating.
+    stg_a = [rd.DeviceCsr(a.rows, a.cols, a.nnz, torch.empty_like(a.row_ptr),
+                          torch.empty_like(a.col_idx), torch.empty_like(a.values))
+             for _ in range(2)]
     rp_h, ci_h, vv_h = (x.cpu().pin_memory() for x in (a.row_ptr, a.col_idx, a.values))
-    b_h = b.cpu().pin_memory() if b is not None else None
-    c_h = torch.empty((m, n), dtype=torch.float32).pin_memory() if cfg["kind"] == "spmm" else \
-        torch.empty(int(Cm.owned_bytes() * 1.05) + 4096, dtype=torch.uint8).pin_memory()
-    a_dev = rd.DeviceCsr(a.rows, a.cols, a.nnz, torch.empty_like(a.row_ptr),
-                         torch.empty_like(a.col_idx), torch.empty_like(a.values))
+    h2d = sum(x.numel() * x.element_size() for x in (rp_h, ci_h, vv_h))
+    if cfg["kind"] == "spmm":
+        b_h = b.cpu().pin_memory()
+        stg_b = [torch.empty_like(b) for _ in range(2)]
+        h2d += b_h.numel() * b_h.element_size()
+        c_h = [torch.empty((m, n), dtype=torch.float32).pin_memory() for _ in range(2)]
+        C2 = [Cm, dm.DistDense(f, m, n, tm, tn, grid, 3)]
+        C2[1].init()
+        d2h = owned_dense_bytes(grid, m, n, tm, tn, rank)
+    else:
+        c_h = torch.empty(int(Cm.owned_bytes() * 1.05) + 4096, dtype=torch.uint8).pin_memory()
     del a, b
-    e2e_steps = max(1, min(args.steps, 3))
-    h2d = d2h = 0
-    e2e_t = []
-    for _ in range(e2e_steps):
-        reset()
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        a_dev.row_ptr.copy_(rp_h, non_blocking=True)
-        a_dev.col_idx.copy_(ci_h, non_blocking=True)
-        a_dev.values.copy_(vv_h, non_blocking=True)
-        torch.cuda.synchronize()
-        A.init_from_device(a_dev)
-        h2d = sum(x.numel() * x.element_size() for x in (rp_h, ci_h, vv_h))
+    up, down = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    e2e_steps = max(4, min(args.steps, 10))
+
+    def upload(s):
+        q = s % 2
+        with torch.cuda.stream(up):
+            stg_a[q].row_ptr.copy_(rp_h, non_blocking=True)
+            stg_a[q].col_idx.copy_(ci_h, non_blocking=True)
+            stg_a[q].values.copy_(vv_h, non_blocking=True)
+            if cfg["kind"] == "spmm":
+                stg_b[q].copy_(b_h, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(up)
+        return ev
+
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ev_in = {0: upload(0)}
+    ev_out = {}
+    for s_ in range(e2e_steps):
+        q = s_ % 2
+        if s_ + 1 < e2e_steps:
+            ev_in[s_ + 1] = upload(s_ + 1)   # queued behind step s_'s upload
+        ev_in[s_].synchronize()
+        A.init_from_device(stg_a[q])
         if cfg["kind"] == "spmm":
-            B.init_from_device(b_h)  # pinned host -> this rank's B tiles
-            h2d += owned_dense_bytes(grid, k, n, tk, tn, rank)
+            B.init_from_device(stg_b[q])
+            if s_ - 2 in ev_out:
+                ev_out[s_ - 2].synchronize()  # C2[q]'s previous download landed
+            C2[q].zero()
+            dm.run_multiply(f, A, B, C2[q], **opts)
+            C2[q].owned_to_host_async(c_h[q], down)
+            ev_out[s_] = torch.cuda.Event()
+            ev_out[s_].record(down)
         else:
-            B.init_from_device(a_dev)
-        dm.run_multiply(f, A, B, Cm, **opts)
-        if cfg["kind"] == "spmm":
-            Cm.owned_to_host(c_h)
-            d2h = owned_dense_bytes(grid, m, n, tm, tn, rank)
-        else:
+            B.init_from_device(stg_a[q])
+            reset()
+            dm.run_multiply(f, A, B, Cm, **opts)
             d2h = Cm.owned_to_host(c_h)
-        torch.cuda.synchronize()
-        barrier()
-        e2e_t.append(time.perf_counter() - t0)
-    e2e_ms = 1e3 * sum(e2e_t) / len(e2e_t)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = 1e3 * (time.perf_counter() - t0) / e2e_steps
     if tdist:
         t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
@@ -525,7 +556,10 @@ def run_ours(args, cfg, dev, rank, world):
         "roofline": roof,
         "e2e": {"value": total_flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                "timer": "host wall clock around upload + run_multiply + download"},
+                "steps": e2e_steps,
+                "timer": "host wall clock over the pipelined steps (pinned H2D of A and B, "
+                         "init_from_device, run_multiply, D2H of C); step s+1's upload "
+                         "overlaps step s's download"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
@@ -815,6 +849,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    # one process per GPU; more ranks than GPUs share them round-robin (a
+    # functional check of a wider layout on a smaller box, not a bench line)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:

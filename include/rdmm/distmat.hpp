@@ -214,17 +214,27 @@ class DistDense {  // distmat.hpp:92-205
   }
   // Copy the caller's owned tiles into a row-major global host array (the
   // device->host half of an end-to-end call; other ranks' tiles untouched).
-  void owned_to_host(RankCtx& ctx, T* global, std::uint64_t ld) {
+  // With `stream` (a caller-owned stream on the rank's device) the copies are
+  // only enqueued there, ordered after the rank's queued compute, and the
+  // call returns at once (the download of one step overlaps the next).
+  void owned_to_host(RankCtx& ctx, T* global, std::uint64_t ld, rdmm_stream_t stream = nullptr) {
+    rdmm_stream_t s = stream ? stream : ctx.stream(0);
+    if (stream) {
+      void* done = nullptr;
+      check(rdmm_event_record(ctx.stream(0), &done), "owned_to_host");
+      check(rdmm_event_wait(done, stream), "owned_to_host");
+      rdmm_event_destroy(done);
+    }
     for (std::uint32_t i = 0; i < geom_.M; ++i)
       for (std::uint32_t j = 0; j < geom_.N; ++j) {
         if (owner(i, j) != ctx.rank()) continue;
         const std::uint32_t r = geom_.tile_rows(i), c = geom_.tile_cols(j);
         T* dst = global + std::uint64_t(i) * geom_.tm * ld + std::uint64_t(j) * geom_.tn;
         check(rdmm_memcpy2d(dst, ld * sizeof(T), fabric_->raw(tile_ptr(i, j), ctx.rank()),
-                            c * sizeof(T), c * sizeof(T), r, ctx.stream(0)),
+                            c * sizeof(T), c * sizeof(T), r, s),
               "owned_to_host");
       }
-    check(rdmm_stream_sync(ctx.stream(0)), "owned_to_host");
+    if (!stream) check(rdmm_stream_sync(ctx.stream(0)), "owned_to_host");
   }
   // B200: zero-tracking so the first product into a fresh tile skips reading C.
   bool tile_is_zero(std::uint32_t i, std::uint32_t j) const { return zero_[geom_.idx(i, j)]; }

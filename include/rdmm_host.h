@@ -60,6 +60,12 @@ int rdmm_h_dense_zero(rdmm_h_matrix* mat);
 int rdmm_h_dense_owned_to_host(rdmm_h_matrix* mat, void* global, uint64_t ld);
 int rdmm_h_sparse_owned_to_host(rdmm_h_matrix* mat, void* buf, uint64_t cap,
                                 uint64_t* bytes);
+/* Asynchronous dense download: the copies are enqueued on `stream` (a
+ * caller-owned cudaStream_t on the local rank's device, one local rank per
+ * process), ordered after the rank's queued compute; returns at once, so a
+ * step's download overlaps the next step's upload and multiply. */
+int rdmm_h_dense_owned_to_host_async(rdmm_h_matrix* mat, void* global, uint64_t ld,
+                                     void* stream);
 /* The compute stream of a local rank (timing events go there). */
 void* rdmm_h_fabric_stream(rdmm_h_fabric* f, uint32_t rank);
 

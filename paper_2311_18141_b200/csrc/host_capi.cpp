@@ -343,6 +343,24 @@ extern "C" int rdmm_h_dense_owned_to_host(rdmm_h_matrix* mat, void* global, uint
   });
 }
 
+extern "C" int rdmm_h_dense_owned_to_host_async(rdmm_h_matrix* mat, void* global, uint64_t ld,
+                                                void* stream) {
+  return guarded([&] {
+    if (mat->kind != 1) throw std::invalid_argument("not a dense matrix");
+    if (!stream) throw std::invalid_argument("owned_to_host_async: a stream is required");
+    auto* s = static_cast<rdmm_stream_t>(stream);
+    if (mat->dtype == 8) {
+      auto& m = *std::get<std::unique_ptr<DistDense<double>>>(mat->m);
+      run_ranks(*mat->fab->f,
+                [&](RankCtx& ctx) { m.owned_to_host(ctx, static_cast<double*>(global), ld, s); });
+    } else {
+      auto& m = *std::get<std::unique_ptr<DistDense<float>>>(mat->m);
+      run_ranks(*mat->fab->f,
+                [&](RankCtx& ctx) { m.owned_to_host(ctx, static_cast<float*>(global), ld, s); });
+    }
+  });
+}
+
 extern "C" int rdmm_h_sparse_owned_to_host(rdmm_h_matrix* mat, void* buf, uint64_t cap,
                                            uint64_t* bytes) {
   return guarded([&] {

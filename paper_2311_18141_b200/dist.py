@@ -64,6 +64,8 @@ _h.rdmm_h_dense_zero.argtypes = [_vp]
 _h.rdmm_h_dense_zero.restype = _int
 _h.rdmm_h_dense_owned_to_host.argtypes = [_vp, _vp, _u64]
 _h.rdmm_h_dense_owned_to_host.restype = _int
+_h.rdmm_h_dense_owned_to_host_async.argtypes = [_vp, _vp, _u64, _vp]
+_h.rdmm_h_dense_owned_to_host_async.restype = _int
 _h.rdmm_h_sparse_owned_to_host.argtypes = [_vp, _vp, _u64, C.POINTER(_u64)]
 _h.rdmm_h_sparse_owned_to_host.restype = _int
 _h.rdmm_h_fabric_stream.argtypes = [_vp, _u32]
@@ -288,6 +290,15 @@ class DistDense(_Mat):
         pinned tensor or numpy array); returns bytes moved."""
         ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
         L.check(_h.rdmm_h_dense_owned_to_host(self._h, ptr, self.n), "owned_to_host")
+
+    def owned_to_host_async(self, out, stream):
+        """Enqueue the D2H of this process's tiles into `out` on `stream` (a
+        torch.cuda.Stream or raw cudaStream_t on the rank's device) after the
+        rank's queued compute, without waiting."""
+        ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+        sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        L.check(_h.rdmm_h_dense_owned_to_host_async(self._h, ptr, self.n, sp),
+                "owned_to_host_async")
 
     def to_global(self):
         out = np.zeros((self.m, self.n), self.dtype)
