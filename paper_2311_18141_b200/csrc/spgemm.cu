@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -117,6 +118,7 @@ template <typename T, int G>
 struct Win {
   uint32_t pre[G];
   uint32_t bs[G];
+  uint32_t be[G];
   T a[G];
   uint32_t sums[32];
 };
@@ -166,6 +168,66 @@ __device__ __forceinline__ void enumerate_row(uint32_t r,
         T v = T(0);
         if (kValues) v = ident ? __ldg(tm.bv + tt) : w.a[lo] * __ldg(tm.bv + tt);
         ins(key, v);
+      }
+      gsync<G>();
+    }
+  }
+}
+
+// Heavy rows, segmented: a window of G A entries is cut into work items of at
+// most kSeg consecutive products of one B row (a block scan of the items per
+// entry); each warp of the CTA (and of the `nparts` CTAs sharing the row)
+// takes whole items, its lanes reading the B-row segment coalesced.  Balanced
+// like the flattened enumeration (R-MAT hub B rows become many items) at one
+// binary search per item instead of one per product.
+constexpr uint32_t kSeg = 256;
+template <typename T, int G, bool kValues, class Ins>
+__device__ __forceinline__ void enumerate_row_seg(uint32_t r, const TermDev<T>* terms,
+                                                  int nterms, Win<T, G>& w, Ins ins,
+                                                  uint32_t part = 0, uint32_t nparts = 1) {
+  const uint32_t tg = threadIdx.x % G, lane = tg & 31, wid = tg >> 5;
+  constexpr uint32_t W = G / 32;
+  for (int t = 0; t < nterms; ++t) {
+    const TermDev<T> tm = terms[t];
+    const bool ident = tm.arp == nullptr;
+    const uint32_t s0 = ident ? 0u : __ldg(tm.arp + r);
+    const uint32_t s1 = ident ? 1u : __ldg(tm.arp + r + 1);
+    for (uint32_t base = s0; base < s1; base += G) {
+      const uint32_t e = base + tg;
+      uint32_t bs = 0, be = 0;
+      T a = T(1);
+      if (e < s1) {
+        const uint32_t k = ident ? r : __ldg(tm.aci + e);
+        if (kValues && !ident) a = __ldg(tm.av + e);
+        bs = __ldg(tm.brp + k);
+        be = __ldg(tm.brp + k + 1);
+      }
+      uint32_t items;
+      const uint32_t ex = gscan<G>((be - bs + kSeg - 1) / kSeg, w.sums, items);
+      w.pre[tg] = ex;
+      w.bs[tg] = bs;
+      w.be[tg] = be;
+      if (kValues) w.a[tg] = a;
+      gsync<G>();
+      const uint32_t nvalid = min(uint32_t(G), s1 - base);
+      for (uint32_t it = part * W + wid; it < items; it += nparts * W) {
+        uint32_t lo = 0, hi = nvalid;
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (w.pre[mid] <= it)
+            lo = mid;
+          else
+            hi = mid;
+        }
+        const uint32_t q0 = w.bs[lo] + (it - w.pre[lo]) * kSeg;
+        const uint32_t q1 = min(q0 + kSeg, w.be[lo]);
+        const T av = kValues ? w.a[lo] : T(1);
+        for (uint32_t q = q0 + lane; q < q1; q += 32) {
+          const uint32_t key = __ldg(tm.bci + q);
+          T v = T(0);
+          if (kValues) v = ident ? __ldg(tm.bv + q) : av * __ldg(tm.bv + q);
+          ins(key, v);
+        }
       }
       gsync<G>();
     }
@@ -321,6 +383,8 @@ __global__ void __launch_bounds__(G == 32 ? 256 : G)
     if (active) {
       if (G >= 512 && !flat)
         enumerate_row_warps<T, G, false>(r, terms, nterms, sym_ins);
+      else if (G >= 128 && flat == 1)
+        enumerate_row_seg<T, G, false>(r, terms, nterms, *win, sym_ins);
       else
         enumerate_row<T, G, false>(r, terms, nterms, *win, sym_ins);
     }
@@ -391,6 +455,8 @@ __global__ void __launch_bounds__(G == 32 ? 256 : G)
     if (active) {
       if (G >= 512 && !flat)
         enumerate_row_warps<T, G, true>(r, terms, nterms, num_ins);
+      else if (G >= 128 && flat == 1)
+        enumerate_row_seg<T, G, true>(r, terms, nterms, *win, num_ins);
       else
         enumerate_row<T, G, true>(r, terms, nterms, *win, num_ins);
     }
@@ -493,6 +559,7 @@ __global__ void __launch_bounds__(kDenseThreads)
   T* wval = reinterpret_cast<T*>(dsm + size_t(kWc) * 4);
   __shared__ Win<T, G> win;
   __shared__ uint32_t slice_count;
+  __shared__ uint32_t coff[G];  // emission: output offset of each 32-word chunk
   const uint32_t part = CL > 1 ? cluster.block_rank() : 0;
   const uint32_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   uint32_t* bm = SBM ? reinterpret_cast<uint32_t*>(dsm + dense_smem_bytes<T>())
@@ -506,8 +573,7 @@ __global__ void __launch_bounds__(kDenseThreads)
   T* dv = dense + size_t(cid) * ncols;
   const uint32_t wper = (nwords + CL - 1) / CL;
   const uint32_t ws0 = min(part * wper, nwords), ws1 = min(ws0 + wper, nwords);
-  const uint32_t tper = (ws1 - ws0 + G - 1) / G;
-  const uint32_t w0 = min(ws0 + threadIdx.x * tper, ws1), w1 = min(w0 + tper, ws1);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t i = threadIdx.x; i < kWc; i += G) {
     wkey[i] = kEmpty;
     wval[i] = ident_val;
@@ -532,45 +598,103 @@ __global__ void __launch_bounds__(kDenseThreads)
         };
     // flat: products spread over every thread of the CTA(s) by a block scan
     // of the B-row lengths (balanced); otherwise whole A entries per warp
-    if (flat)
+    if (flat == 2)
       enumerate_row<T, G, true>(r, terms, nterms, win, dense_ins, part, CL);
+    else if (flat)
+      enumerate_row_seg<T, G, true>(r, terms, nterms, win, dense_ins, part, CL);
     else
       enumerate_row_warps<T, G, true>(r, terms, nterms, dense_ins, part, CL);
+    // CL = 1, no flush: a column's products all went to the cache slot it
+    // claimed first or all to the dense array (slots are never evicted), so
+    // the emission reads each column from where it accumulated.  CL > 1: the
+    // CTAs' caches overlap; flush them into the dense array.
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < kWc; i += G) {  // flush the cache
-      const uint32_t key = wkey[i];
-      if (key != kEmpty) {
-        atomicAdd(dv + key, wval[i]);
-        wkey[i] = kEmpty;
-        wval[i] = ident_val;
+    if constexpr (CL > 1) {
+      for (uint32_t i = threadIdx.x; i < kWc; i += G) {
+        const uint32_t key = wkey[i];
+        if (key != kEmpty) {
+          atomicAdd(dv + key, wval[i]);
+          wkey[i] = kEmpty;
+          wval[i] = ident_val;
+        }
       }
     }
     __threadfence();
     if constexpr (CL > 1) cluster.sync(); else __syncthreads();
-    uint32_t c = 0;
-    for (uint32_t w = w0; w < w1; ++w) c += __popc(ldbm(w));
-    uint32_t total;
-    const uint32_t off = gscan<G>(c, win.sums, total);
+    // Emission in column order, balanced over the threads: the slice's
+    // words form chunks of 32; a block scan of the chunk counts gives each
+    // chunk's output offset, and the warps take chunks interleaved (R-MAT's
+    // output columns crowd the low words, which a contiguous word range per
+    // thread turned into a barrier wait behind a few threads), one word per
+    // lane with a warp scan for the positions inside the chunk.
+    const uint32_t nchunk = (ws1 - ws0 + 31) / 32;
     uint32_t base = 0;
     if constexpr (CL > 1) {
-      if (threadIdx.x == 0) slice_count = total;
+      uint32_t c = 0;
+      for (uint32_t w = ws0 + threadIdx.x; w < ws1; w += G) c += __popc(ldbm(w));
+      const uint32_t tot = gsum<G>(c, win.sums);
+      if (threadIdx.x == 0) slice_count = tot;
       cluster.sync();
       for (uint32_t q = 0; q < part; ++q) base += *cluster.map_shared_rank(&slice_count, q);
     }
-    uint32_t pos = crp[r] + base + off;
-    for (uint32_t w = w0; w < w1; ++w) {
-      uint32_t bits = ldbm(w);
-      if (!bits) continue;
-      bm[w] = 0;
-      while (bits) {
-        const uint32_t b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const uint32_t col = w * 32 + b;
-        cci[pos] = col;
-        cv[pos] = __ldcg(dv + col);
-        dv[col] = ident_val;
-        ++pos;
+    uint32_t run = crp[r] + base;
+    for (uint32_t g0 = 0; g0 < nchunk; g0 += G) {
+      const uint32_t ch = g0 + threadIdx.x;
+      uint32_t c = 0;
+      if (ch < nchunk) {
+        const uint32_t wa = ws0 + ch * 32, wb = min(wa + 32, ws1);
+        for (uint32_t w = wa; w < wb; ++w) c += __popc(ldbm(w));
       }
+      uint32_t total;
+      coff[threadIdx.x] = gscan<G>(c, win.sums, total);
+      __syncthreads();
+      for (uint32_t j = warp; j < uint32_t(G) && g0 + j < nchunk; j += G / 32) {
+        const uint32_t w = ws0 + (g0 + j) * 32 + lane;
+        uint32_t bits = w < ws1 ? ldbm(w) : 0u;
+        const uint32_t cnt = __popc(bits);
+        uint32_t inc = cnt;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
+          if (lane >= uint32_t(off)) inc += y;
+        }
+        uint32_t pos = run + coff[j] + inc - cnt;
+        if (bits) bm[w] = 0;
+        while (bits) {  // eight columns per round: their value loads overlap
+          uint32_t cols[8];
+          T vals[8];
+          int nb = 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            cols[q] = w * 32 + (bits ? __ffs(bits) - 1 : 0u);
+            if (bits) {
+              bits &= bits - 1;
+              nb = q + 1;
+            }
+          }
+          bool cached[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint32_t sl = hslot(cols[q], LOG2W);
+            cached[q] = CL == 1 && q < nb && wkey[sl] == cols[q];
+            if (q < nb) vals[q] = cached[q] ? wval[sl] : __ldcg(dv + cols[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (q < nb) {
+              cci[pos + q] = cols[q];
+              cv[pos + q] = vals[q];
+              if (!cached[q]) dv[cols[q]] = ident_val;
+            }
+          pos += uint32_t(nb);
+        }
+      }
+      run += total;
+      __syncthreads();
+    }
+    for (uint32_t i = threadIdx.x; i < kWc; i += G) {  // reset the cache
+      wkey[i] = kEmpty;
+      wval[i] = ident_val;
     }
     __threadfence();
     if constexpr (CL > 1) cluster.sync(); else __syncthreads();
@@ -660,21 +784,51 @@ inline int dense_cl() {
   }();
   return v;
 }
-// Heavy-row product enumeration for the CTA tiers (G >= 512) and the dense
-// tier: 1 (default) = block-balanced flattened products (a block scan of the
-// B-row lengths per window of A entries); 0 = whole A entries per warp, which
-// leaves warps waiting at the row barrier behind R-MAT hub B rows (ncu:
-// barrier stalls 92 cycles/instr; s20 283 ms vs 207 ms).  RDMM_SPGEMM_FLAT
-// overrides (dev switch).
+// Product enumeration for the CTA tiers (G >= 128) and the dense tier:
+// 2 (default) = flattened products (a block scan of the B-row lengths per
+// window of A entries, a binary search per product); 1 = segmented items
+// (kSeg products of one B row per warp, one search per item: fewer
+// instructions but measured 6% slower at s20, 141 vs 133 ms); 0 = whole A
+// entries per warp, which leaves warps waiting at the row barrier behind
+// R-MAT hub B rows (ncu: barrier stalls 92 cycles/instr; s20 283 ms vs
+// 207 ms).  RDMM_SPGEMM_FLAT overrides (a measurement switch).
 inline int dense_flat() {
   static const int v = [] {
     const char* e = std::getenv("RDMM_SPGEMM_FLAT");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 2;
   }();
   return v;
 }
 inline uint32_t dense_rows_in_flight(uint32_t rows, int cl) {
   return std::max<uint32_t>(1, std::min<uint32_t>(rows, uint32_t(num_sms()) / cl));
+}
+// Numeric dense tier: rows in flight (one per SM; limiting them so that the
+// dense arrays stay L2-resident measured 4.6x slower at 18 rows: the tier is
+// bound by per-row work, not by DRAM).  RDMM_SPGEMM_DENSE_SLOTS overrides (a
+// measurement switch).
+inline uint32_t dense_num_slots(uint32_t rows, size_t bytes_per_row, int cl) {
+  static const int env = [] {
+    const char* e = std::getenv("RDMM_SPGEMM_DENSE_SLOTS");
+    return e ? std::atoi(e) : 0;
+  }();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+  (void)l2;
+  (void)bytes_per_row;
+  uint32_t fit = env > 0 ? uint32_t(env) : uint32_t(num_sms());
+  return std::max<uint32_t>(1, std::min<uint32_t>({rows, fit, uint32_t(num_sms()) / cl}));
+}
+// Side stream per device for tiers that run concurrently with the others.
+inline cudaStream_t side_stream() {
+  static cudaStream_t ss[64] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ss[dev & 63]) cudaStreamCreateWithFlags(&ss[dev & 63], cudaStreamNonBlocking);
+  return ss[dev & 63];
 }
 
 template <typename T, int CL>
@@ -683,7 +837,7 @@ int launch_dense_num(uint32_t slots, const uint32_t* list, uint32_t count,
                      uint32_t* bm, T* dense, uint32_t nwords, uint32_t ncols, T ident,
                      cudaStream_t s) {
   // static shared memory of the kernel: Win<T, G> + a counter
-  const size_t stat = sizeof(Win<T, kDenseThreads>) + 64;
+  const size_t stat = sizeof(Win<T, kDenseThreads>) + 64 + kDenseThreads * 4;
   const bool sbm = CL == 1 && dense_smem_bytes<T>() + size_t(nwords) * 4 + stat <= 226 * 1024;
   auto fn = sbm ? k_dense_num<T, CL, true> : k_dense_num<T, CL, false>;
   const size_t sm = dense_smem_bytes<T>() + (sbm ? size_t(nwords) * 4 : 0);
@@ -941,6 +1095,17 @@ int numeric_impl(rdmm_spgemm_plan* P, uint32_t* cci, T* cv, cudaStream_t s) {
   // (0xFFFFFFFF) still sorts last once truncated to them
   int key_bits = 1;
   while (key_bits < 32 && (uint64_t(1) << key_bits) <= P->ncols) ++key_bits;
+  // the dense tier (few SMs, L2-resident arrays) runs on a side stream beside
+  // the hash tiers; rows of different tiers are disjoint
+  cudaStream_t main_s = s;
+  cudaStream_t ds = s;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  if (c[5]) {
+    ds = side_stream();
+    RDMM_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    RDMM_CUDA_TRY(cudaEventRecord(fork, main_s));
+    RDMM_CUDA_TRY(cudaStreamWaitEvent(ds, fork, 0));
+  }
   int rc = 0;
   rc |= launch_num_hash<T, 64, 32>(L(0), c[0], td, nt, crp, cci, cv, ident, key_bits, s);
   rc |= launch_num_hash<T, 512, 128>(L(1), c[1], td, nt, crp, cci, cv, ident, key_bits, s);
@@ -951,10 +1116,13 @@ int numeric_impl(rdmm_spgemm_plan* P, uint32_t* cci, T* cv, cudaStream_t s) {
   if (c[5]) {
     const uint32_t nwords = uint32_t(ceil_div(P->ncols, 32));
     const int cl = dense_cl();
-    const uint32_t blocks = dense_rows_in_flight(c[5], cl);
-    RDMM_CUDA_TRY(P->bitmaps.ensure(size_t(blocks) * nwords * 4, s));
+    const uint32_t blocks = dense_num_slots(c[5], size_t(P->ncols) * sizeof(T), cl);
+    s = ds;
+    RDMM_CUDA_TRY(P->bitmaps.ensure(size_t(blocks) * nwords * 4, main_s));
+    RDMM_CUDA_TRY(P->dense.ensure(size_t(blocks) * P->ncols * sizeof(T), main_s));
+    RDMM_CUDA_TRY(cudaEventRecord(fork, main_s));  // the buffers exist
+    RDMM_CUDA_TRY(cudaStreamWaitEvent(s, fork, 0));
     RDMM_CUDA_TRY(cudaMemsetAsync(P->bitmaps.p, 0, size_t(blocks) * nwords * 4, s));
-    RDMM_CUDA_TRY(P->dense.ensure(size_t(blocks) * P->ncols * sizeof(T), s));
     const size_t nd = size_t(blocks) * P->ncols;
     count_launch();
     k_fill<T><<<unsigned(std::min<uint64_t>(ceil_div(nd, 256), 4096)), 256, 0, s>>>(
@@ -969,6 +1137,11 @@ int numeric_impl(rdmm_spgemm_plan* P, uint32_t* cci, T* cv, cudaStream_t s) {
       default: rc2 = launch_dense_num<T, 1>(blocks, L(5), c[5], td, nt, crp, cci, cv, bm, dn, nwords, P->ncols, ident, s);
     }
     if (rc2) return rc2;
+    RDMM_CUDA_TRY(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    RDMM_CUDA_TRY(cudaEventRecord(join, ds));
+    RDMM_CUDA_TRY(cudaStreamWaitEvent(main_s, join, 0));
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
   }
   RDMM_CUDA_TRY(cudaGetLastError());
   return RDMM_OK;
