@@ -139,6 +139,17 @@ def p2p_peak():
     return 900.0, "nominal NVLink 5 per direction"
 
 
+def cdev():
+    """Device of the small tensors of the bench's own collectives: the GPU
+    under NCCL, the host under gloo (more ranks than GPUs)."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.is_initialized() and dist.get_backend() == "gloo":
+        return torch.device("cpu")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
 def verify(args, cfg, dev, rank, world, A, Cm, grid, tiles, tdist):
     """Compare the distributed result with the single-GPU kernel on the
     global operands (itself pinned to the oracle by tests/): SpMM owned C
@@ -173,7 +184,7 @@ def verify(args, cfg, dev, rank, world, A, Cm, grid, tiles, tdist):
                       np.array_equal(vv, gvv))
         what = "gathered C row_ptr/col_idx/values == single-GPU spgemm_local(A, A) (exact)"
     if tdist:
-        t = torch.tensor([0 if ok else 1], device=dev)
+        t = torch.tensor([0 if ok else 1], device=cdev())
         tdist.all_reduce(t)
         ok = int(t[0]) == 0
     return {"ok": ok, "checked": what}
@@ -386,10 +397,10 @@ def run_ours(args, cfg, dev, rank, world):
     barrier()
     sf = rep_t.stage_flops
     sm_ = rep_t.stage_ms if rep_t.stage_ms is not None else np.zeros(sf.shape)
-    width = torch.tensor([sf.shape[1]], device=dev, dtype=torch.int64)
+    width = torch.tensor([sf.shape[1]], device=cdev(), dtype=torch.int64)
     if tdist:
         tdist.all_reduce(width, op=tdist.ReduceOp.MAX)
-    tabs = torch.zeros((2, sf.shape[0], int(width[0])), device=dev, dtype=torch.float64)
+    tabs = torch.zeros((2, sf.shape[0], int(width[0])), device=cdev(), dtype=torch.float64)
     tabs[0, :, :sf.shape[1]] = torch.as_tensor(sf, dtype=torch.float64)
     tabs[1, :, :sm_.shape[1]] = torch.as_tensor(sm_, dtype=torch.float64)
     if tdist:
@@ -403,12 +414,12 @@ def run_ours(args, cfg, dev, rank, world):
                                "(cudaEvents, RankStats::stage_ms)"}
     nvlink = None
     if tdist:  # NVLink bytes per rank per step, against the measured P2P bandwidth
-        nv = torch.tensor([nvl_local], device=dev, dtype=torch.float64)
+        nv = torch.tensor([nvl_local], device=cdev(), dtype=torch.float64)
         alln = [torch.zeros_like(nv) for _ in range(world)]
         tdist.all_gather(alln, nv)
         nvl = [float(x[0]) for x in alln]
     if tdist:  # max over ranks of the device time; flops summed over ranks
-        t = torch.tensor([ms_local, float(flops_local), float(steals)], device=dev,
+        t = torch.tensor([ms_local, float(flops_local), float(steals)], device=cdev(),
                          dtype=torch.float64)
         tmax = t[:1].clone()
         tdist.all_reduce(tmax, op=tdist.ReduceOp.MAX)
@@ -525,7 +536,7 @@ def run_ours(args, cfg, dev, rank, world):
     barrier()
     e2e_ms = 1e3 * (time.perf_counter() - t0) / e2e_steps
     if tdist:
-        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([e2e_ms], device=cdev(), dtype=torch.float64)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         e2e_ms = float(t[0])
 
@@ -855,7 +866,10 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        torch.distributed.init_process_group("nccl", device_id=dev)
+        if world <= torch.cuda.device_count():
+            torch.distributed.init_process_group("nccl", device_id=dev)
+        else:  # NCCL refuses two ranks on one GPU
+            torch.distributed.init_process_group("gloo")
     if args.variant == "summa_nccl":
         out = run_summa_nccl(args, cfg, dev, rank, world)
     else:
