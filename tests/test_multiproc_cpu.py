@@ -99,10 +99,11 @@ def test_bench_session_and_layout():
         grid = None
         mtiles = ktiles = ntiles = 0
 
+    # SpMM: 1 x P column split (every rank all rows, N/P columns, K = P)
     (pr, pc), tiles = bench.layout(bench.CONFIGS["cfg3"], 8, A)
-    assert (pr, pc) == (8, 1) and tuple(tiles) == (524288, 524288, 128)
+    assert (pr, pc) == (1, 8) and tuple(tiles) == (4194304, 524288, 16)
     (pr, pc), tiles = bench.layout(bench.CONFIGS["cfg5"], 4, A)
-    assert (pr, pc) == (2, 2) and tuple(tiles) == (2097152, 2097152, 128)
+    assert (pr, pc) == (1, 4) and tuple(tiles) == (4194304, 1048576, 64)
     (pr, pc), tiles = bench.layout(bench.CONFIGS["cfg3"], 1, A)
     assert (pr, pc) == (1, 1) and tuple(tiles) == (4194304, 4194304, 128)
     (pr, pc), tiles = bench.layout(bench.CONFIGS["cfg4"], 4, A)
