@@ -286,44 +286,71 @@ FlopMeter spmm_local(DevCsrView<T> a, DevDenseConstView<T> b, DevDenseView<T> c,
 }
 
 // Fused stationary-C product of one tile column: c += sum_k a_k * b_k in ONE
-// pass over c (the K A tiles are concatenated side by side on the device,
-// B is read as K row segments).  col_stride = rows of each b_k but the last.
+// pass over c (the K A tiles are concatenated side by side on the device).
+// The tiles come in accumulation order with their natural k index `knat`;
+// concatenated column indices are the natural ones (knat[k] * col_stride +
+// c), so when the B tiles form one contiguous panel in natural order
+// (DistDense's placement) B is read directly, else through the segment
+// table.  `atomic`: accumulate into c with red.global.add (narrow rows).
 template <typename T>
 FlopMeter spmm_fused(rdmm_fabric* f, std::uint32_t rank, const std::vector<DevCsrView<T>>& a,
-                     const std::vector<DevDenseConstView<T>>& b, std::uint64_t col_stride,
-                     DevDenseView<T> c, rdmm_stream_t stream, bool c_zero = false) {
+                     const std::vector<DevDenseConstView<T>>& b,
+                     const std::vector<std::uint32_t>& knat, std::uint64_t col_stride,
+                     DevDenseView<T> c, rdmm_stream_t stream, bool c_zero = false,
+                     bool atomic = false) {
   const std::size_t K = a.size();
-  if (K == 0 || b.size() != K || K > 16) throw std::invalid_argument("spmm_fused: 1..16 tiles");
-  if (K == 1) return spmm_local<T>(a[0], b[0], c, stream, c_zero);
+  if (K == 0 || b.size() != K || K > 16 || knat.size() != K)
+    throw std::invalid_argument("spmm_fused: 1..16 tiles");
+  if (K == 1) return spmm_local<T>(a[0], b[0], c, stream, c_zero, atomic);
   std::uint64_t nnz = 0;
+  std::uint32_t kmax = 0;
+  for (auto k : knat) kmax = std::max(kmax, k);
   std::vector<const index_t*> rp(K), ci(K);
-  std::vector<std::uint64_t> tn(K);
-  std::vector<const void*> vv(K), bs(K);
+  std::vector<const void*> vv(K);
+  std::vector<const void*> bs(kmax + 1, nullptr);
+  std::vector<std::uint64_t> coff(K);
   for (std::size_t k = 0; k < K; ++k) {
     if (a[k].rows != c.rows || a[k].cols != b[k].rows || b[k].cols != c.cols ||
-        b[k].ld != b[0].ld || b[k].rows > col_stride)
+        b[k].ld != b[0].ld || b[k].rows > col_stride || bs[knat[k]])
       throw dimension_error("spmm_fused: dimension mismatch");
     nnz += a[k].nnz;
-    tn[k] = a[k].nnz;
     rp[k] = a[k].row_ptr;
     ci[k] = a[k].col_idx;
     vv[k] = a[k].values;
-    bs[k] = b[k].values;
+    bs[knat[k]] = b[k].values;
+    coff[k] = std::uint64_t(knat[k]) * col_stride;
   }
+  // one contiguous panel over natural k = 0..kmax (every segment present)?
+  bool panel = true;
+  for (std::size_t k = 0; k <= kmax; ++k)
+    panel &= bs[k] != nullptr && static_cast<const T*>(bs[k]) ==
+                                     static_cast<const T*>(bs[0]) + k * col_stride * b[0].ld;
   DevBuffer crp(f, rank, (std::uint64_t(c.rows) + 1) * sizeof(index_t), stream);
-  DevBuffer cci(f, rank, nnz * sizeof(index_t), stream);
-  DevBuffer cvv(f, rank, nnz * sizeof(T), stream);
-  check(rdmm_csr_concat_cols(dtype_bytes<T>(), c.rows, std::uint32_t(K), rp.data(), ci.data(),
-                             vv.data(), tn.data(), col_stride, static_cast<index_t*>(crp.get()),
-                             static_cast<index_t*>(cci.get()), cvv.get(), stream),
+  DevBuffer cci(f, rank, std::max<std::uint64_t>(nnz, 1) * sizeof(index_t), stream);
+  DevBuffer cvv(f, rank, std::max<std::uint64_t>(nnz, 1) * sizeof(T), stream);
+  check(rdmm_csr_concat_cols_rows(dtype_bytes<T>(), 0, c.rows, std::uint32_t(K), rp.data(),
+                                  ci.data(), vv.data(), col_stride, coff.data(),
+                                  static_cast<index_t*>(crp.get()),
+                                  static_cast<index_t*>(cci.get()), cvv.get(), stream),
         "spmm_fused concat");
+  const unsigned flags = (c_zero ? RDMM_SPMM_C_ZERO : 0u) | (atomic ? RDMM_SPMM_ATOMIC : 0u);
   std::uint64_t fl = 0;
-  check(rdmm_spmm_csr_seg(dtype_bytes<T>(), c.rows, c.cols, nnz,
-                          static_cast<const index_t*>(crp.get()),
-                          static_cast<const index_t*>(cci.get()), cvv.get(), bs.data(),
-                          std::uint32_t(K), std::uint32_t(col_stride), b[0].ld, c.values, c.ld,
-                          c_zero ? RDMM_SPMM_C_ZERO : 0u, nullptr, 0, stream, &fl),
-        "spmm_fused");
+  if (panel) {
+    check(rdmm_spmm_csr_ex(dtype_bytes<T>(), c.rows, std::uint32_t(col_stride * (kmax + 1)),
+                           c.cols, nnz, static_cast<const index_t*>(crp.get()),
+                           static_cast<const index_t*>(cci.get()), cvv.get(), bs[0], b[0].ld,
+                           c.values, c.ld, flags, nullptr, 0, stream, &fl),
+          "spmm_fused");
+  } else {
+    for (auto& p : bs)  // unused segments: any valid pointer (never indexed)
+      if (!p) p = b[0].values;
+    check(rdmm_spmm_csr_seg(dtype_bytes<T>(), c.rows, c.cols, nnz,
+                            static_cast<const index_t*>(crp.get()),
+                            static_cast<const index_t*>(cci.get()), cvv.get(), bs.data(),
+                            kmax + 1, std::uint32_t(col_stride), b[0].ld, c.values, c.ld, flags,
+                            nullptr, 0, stream, &fl),
+          "spmm_fused");
+  }
   FlopMeter m;
   m.flops = fl;
   m.output_nnz = std::uint64_t(c.rows) * c.cols;

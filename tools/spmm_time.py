@@ -20,11 +20,47 @@ ap.add_argument("--er", action="store_true")
 ap.add_argument("--czero", type=int, default=0)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--tag", default="")
+ap.add_argument("--coltiles", type=int, default=0,
+                help="time each of K column tiles of A separately (the 1xK passes)")
+ap.add_argument("--atomic", type=int, default=0)
 args = ap.parse_args()
 if args.er:
     a = rd.uniform_tiles(1 << args.scale, 1 << args.scale, 1, 16.0 / (1 << args.scale), 1)
 else:
     a = rd.rmat(args.scale, args.ef, seed=1)
+if args.coltiles:
+    from paper_2311_18141_b200 import _lib as L
+    from paper_2311_18141_b200.tile import extract_tile
+    import ctypes as C
+    K = args.coltiles
+    tk = a.cols // K
+    for n in args.n:
+        b = rd.random_dense(a.cols, n, 2)
+        c = torch.zeros((a.rows, n), device="cuda")
+        for k in range(K):
+            t = extract_tile(a, 0, a.rows, k * tk, tk)
+            bk = b[k * tk:(k + 1) * tk]
+            flags = (L.SPMM_C_ZERO if args.czero else 0) | (4 if args.atomic else 0)
+            fl = C.c_uint64(0)
+            def run():
+                L.check(L.rdmm_spmm_csr_ex(4, t.rows, t.cols, n, t.nnz, t.row_ptr.data_ptr(),
+                                           t.col_idx.data_ptr(), t.values.data_ptr(),
+                                           bk.data_ptr(), n, c.data_ptr(), n, flags, None, 0,
+                                           None, C.byref(fl)), "spmm")
+            for _ in range(2):
+                run()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.iters):
+                run()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / args.iters
+            nonempty = int((torch.diff(t.row_ptr.long()) > 0).sum())
+            print(json.dumps({"K": K, "k": k, "n": n, "nnz": t.nnz, "nonempty_rows": nonempty,
+                              "ms": ms, "atomic": args.atomic, "czero": args.czero}), flush=True)
+    sys.exit(0)
 for n in args.n:
     b = rd.random_dense(a.cols, n, 2)
     c = torch.zeros((a.rows, n), device="cuda")
