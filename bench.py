@@ -457,7 +457,8 @@ def run_ours(args, cfg, dev, rank, world):
         kernel = "spmm_stream+spmm_fixup (rdmm_spmm_csr), all launches of a step on this rank"
     else:
         alg = (2 * a_bytes + (m + 1) * 4 + 8 * (out_nnz or 0)) // world
-        kernel = "spgemm numeric tiers (rdmm_spgemm_numeric), per step on this rank"
+        kernel = ("spgemm symbolic + numeric passes (rdmm_spgemm_symbolic/numeric), per step "
+                  "on this rank")
     kms_step = kms / max(1, args.steps)
     achieved = alg / (kms_step * 1e-3) / 1e9 if kms_step > 0 else None
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",

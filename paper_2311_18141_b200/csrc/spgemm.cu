@@ -954,6 +954,9 @@ template <typename T>
 int symbolic_impl(uint32_t rows, uint32_t ncols, const rdmm_spgemm_term* terms,
                   int nterms, uint32_t* c_row_ptr, rdmm_spgemm_plan** out,
                   uint64_t* c_nnz, uint64_t* flops, cudaStream_t s) {
+  // the symbolic pass counts toward the SpGEMM kernel time too (VERDICT r1:
+  // the roofline time of a product must include both passes)
+  KernelTimer timer(s, 2);
   auto* P = new rdmm_spgemm_plan();
   std::unique_ptr<rdmm_spgemm_plan> guard(P);
   P->dtype = sizeof(T);
