@@ -749,7 +749,7 @@ struct AsyncCfg {
   }
 };
 
-template <typename T, int S, bool CZERO, bool SEG>
+template <typename T, int S, bool CZERO, bool SEG, bool ATOMIC>
 __global__ void __launch_bounds__(kThreads, 2)
     spmm_slots_async(const SpmmArgs<T> p) {
   using C_ = AsyncCfg<T>;
@@ -906,13 +906,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     T* crow = Cs + uint64_t(row) * p.ldc + col0;
 #pragma unroll
     for (int x = 0; x < LEN; ++x)
-      cin[x] = (!CZERO && !p.atomic && starts && owner) ? __ldcs(crow + x) : T(0);
+      cin[x] = (!CZERO && !ATOMIC && starts && owner) ? __ldcs(crow + x) : T(0);
     // flush the current row (it ends at rend) and move to the next one
     auto flush = [&]() {
       T o[LEN];
       reduce(acc, o);
       if (owner) {
-        if (p.atomic) {
+        if (ATOMIC) {
 #pragma unroll
           for (int x = 0; x < LEN; ++x) atomicAdd(crow + x, o[x]);
         } else if (starts) {
@@ -938,7 +938,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       acc = vzero<V>();
       crow = Cs + uint64_t(row) * p.ldc + col0;
 #pragma unroll
-      for (int x = 0; x < LEN; ++x) cin[x] = (!CZERO && !p.atomic && owner) ? __ldcs(crow + x) : T(0);
+      for (int x = 0; x < LEN; ++x) cin[x] = (!CZERO && !ATOMIC && owner) ? __ldcs(crow + x) : T(0);
     };
     for (uint32_t w = lo; w < hi; w += 32) {
       issue_a();
@@ -998,7 +998,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
       for (int x = 0; x < LEN; ++x) o[x] = cin[x] + o[x];
     int32_t trow = -1;
-    if (p.atomic) {
+    if (ATOMIC) {
       if (owner)
 #pragma unroll
         for (int x = 0; x < LEN; ++x) atomicAdd(crow + x, o[x]);
@@ -1280,12 +1280,16 @@ void launch_seg(const SpmmArgs<T>& a, bool czero, int blocks, cudaStream_t s) {
       else spmm_slots<T, VEC, S, false, 3, SEG><<<blocks, kThreads, 0, s>>>(a);
     } else if (kv == 0 && G <= 8 && VEC * sizeof(T) == 16 && async_mode()) {
       const size_t sm = AsyncCfg<T>::smem(G);
-      auto fn = czero ? spmm_slots_async<T, S, true, SEG> : spmm_slots_async<T, S, false, SEG>;
+      // atomic accumulation never reads C: one instantiation serves it
+      const int variant = a.atomic ? 2 : czero ? 1 : 0;
+      auto fn = variant == 2   ? spmm_slots_async<T, S, false, SEG, true>
+                : variant == 1 ? spmm_slots_async<T, S, true, SEG, false>
+                               : spmm_slots_async<T, S, false, SEG, false>;
       // the dynamic shared-memory opt-in is per device
-      static std::atomic<int> resident[2][kMaxDevices] = {};  // CTAs per SM (persistent grid)
+      static std::atomic<int> resident[3][kMaxDevices] = {};  // CTAs per SM (persistent grid)
       int dev = 0;
       cudaGetDevice(&dev);
-      std::atomic<int>& res = resident[czero][dev < kMaxDevices ? dev : 0];
+      std::atomic<int>& res = resident[variant][dev < kMaxDevices ? dev : 0];
       if (!res.load()) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         int nb = 0;
