@@ -492,7 +492,8 @@ template <typename T>
 DevCsrTile<T> spgemm_terms(rdmm_fabric* f, std::uint32_t rank, index_t rows, index_t cols,
                            const std::vector<SpgemmTerm<T>>& terms, rdmm_stream_t stream,
                            FlopMeter* meter = nullptr,
-                           std::vector<std::uint64_t>* term_flops = nullptr) {
+                           std::vector<std::uint64_t>* term_flops = nullptr,
+                           bool deterministic = false) {
   std::vector<rdmm_spgemm_term> tt(terms.size());
   for (std::size_t i = 0; i < terms.size(); ++i) {
     const auto& t = terms[i];
@@ -512,8 +513,9 @@ DevCsrTile<T> spgemm_terms(rdmm_fabric* f, std::uint32_t rank, index_t rows, ind
   out.nnz = nnz;
   out.col_idx = DevBuffer(f, rank, nnz * sizeof(index_t), stream);
   out.values = DevBuffer(f, rank, nnz * sizeof(T), stream);
-  int rc = rdmm_spgemm_numeric(plan, static_cast<index_t*>(out.col_idx.get()),
-                               out.values.get(), stream);
+  int rc = rdmm_spgemm_numeric_ex(plan, static_cast<index_t*>(out.col_idx.get()),
+                                  out.values.get(),
+                                  deterministic ? RDMM_SPGEMM_DETERMINISTIC : 0u, stream);
   if (term_flops && rc == RDMM_OK) {
     term_flops->assign(terms.size(), 0);
     rdmm_spgemm_plan_term_flops(plan, term_flops->data());
@@ -531,10 +533,12 @@ DevCsrTile<T> spgemm_terms(rdmm_fabric* f, std::uint32_t rank, index_t rows, ind
 template <typename T>
 std::pair<DevCsrTile<T>, FlopMeter> spgemm_local(rdmm_fabric* f, std::uint32_t rank,
                                                  DevCsrView<T> a, DevCsrView<T> b,
-                                                 rdmm_stream_t stream) {
+                                                 rdmm_stream_t stream,
+                                                 bool deterministic = false) {
   if (a.cols != b.rows) throw dimension_error("spgemm_local: dimension mismatch");
   FlopMeter m;
-  auto c = spgemm_terms<T>(f, rank, a.rows, b.cols, {{a, b, false}}, stream, &m);
+  auto c = spgemm_terms<T>(f, rank, a.rows, b.cols, {{a, b, false}}, stream, &m, nullptr,
+                           deterministic);
   return {std::move(c), m};
 }
 

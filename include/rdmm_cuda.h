@@ -163,6 +163,14 @@ int rdmm_spgemm_symbolic(uint32_t rows, uint32_t ncols, int dtype_bytes,
                          rdmm_stream_t stream);
 int rdmm_spgemm_numeric(rdmm_spgemm_plan* plan, uint32_t* c_col_idx,
                         void* c_val, rdmm_stream_t stream);
+/* Numeric pass with flags.  RDMM_SPGEMM_DETERMINISTIC: values are the
+ * reference's for ANY inputs, bitwise and run to run -- each output is the
+ * fma chain of its products in the reference's loop order (tile.hpp:225-237),
+ * the terms combined in order like successive csr_adds (tile.hpp:257-288);
+ * products are expanded and stably sorted per row batch (slower; opt-in). */
+#define RDMM_SPGEMM_DETERMINISTIC 1u
+int rdmm_spgemm_numeric_ex(rdmm_spgemm_plan* plan, uint32_t* c_col_idx, void* c_val,
+                           unsigned flags, rdmm_stream_t stream);
 void rdmm_spgemm_plan_destroy(rdmm_spgemm_plan* plan);
 /* FlopMeter flops of each term (identity terms count 0). */
 int rdmm_spgemm_plan_term_flops(const rdmm_spgemm_plan* plan, uint64_t* out);

@@ -106,6 +106,8 @@ class SpgemmTerm(C.Structure):
 rdmm_spgemm_symbolic = _fn("rdmm_spgemm_symbolic", [u32, u32, cint, P(SpgemmTerm), cint, vp,
                                                     P(vp), P(u64), P(u64), vp])
 rdmm_spgemm_numeric = _fn("rdmm_spgemm_numeric", [vp, vp, vp, vp])
+rdmm_spgemm_numeric_ex = _fn("rdmm_spgemm_numeric_ex", [vp, vp, vp, u32, vp])
+SPGEMM_DETERMINISTIC = 1
 rdmm_spgemm_plan_destroy = _fn("rdmm_spgemm_plan_destroy", [vp], None)
 rdmm_spgemm_plan_info = _fn("rdmm_spgemm_plan_info", [vp, P(u32), P(u32)])
 rdmm_dense_add_into_f32 = _fn("rdmm_dense_add_into_f32", [u32, u32, vp, u64, vp, u64, vp])

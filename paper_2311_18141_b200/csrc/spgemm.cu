@@ -28,6 +28,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <numeric>
 #include <vector>
 
 #include "common.cuh"
@@ -860,6 +861,118 @@ int launch_dense_num(uint32_t slots, const uint32_t* list, uint32_t count,
   return RDMM_OK;
 }
 
+// ------------------------------------------------------------ deterministic
+//
+// Opt-in numeric pass with the reference's floating-point result for ANY
+// values (RDMM_SPGEMM_DETERMINISTIC): every product of a batch of rows is
+// expanded in enumeration order (term, A entry, B entry -- the reference's
+// loop order, tile.hpp:225-237) as (key = row|col|term, a, b), a stable radix
+// sort groups equal keys keeping that order, and one thread per output entry
+// folds its run: within a product term sum = fma(a, b, sum) from +0 in order
+// (tile.hpp:232); identity terms contribute their value as-is; term results
+// combine in term order, first value copied, later ones added -- csr_add
+// (tile.hpp:257-288) applied per term as stationary-C does (algos.hpp:254).
+template <typename T>
+struct AB {
+  T a, b;
+};
+
+template <typename T>
+__global__ void k_det_count(uint32_t r0, uint32_t rows, const TermDev<T>* terms, int nterms,
+                            uint64_t* cnt) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < rows;
+       w += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t r = r0 + w;
+    unsigned long long n = 0;
+    for (int t = 0; t < nterms; ++t) {
+      const TermDev<T> tm = terms[t];
+      if (tm.arp == nullptr) {
+        if (lane == 0) n += __ldg(tm.brp + r + 1) - __ldg(tm.brp + r);
+      } else {
+        for (uint32_t e = __ldg(tm.arp + r) + lane; e < __ldg(tm.arp + r + 1); e += 32) {
+          const uint32_t k = __ldg(tm.aci + e);
+          n += __ldg(tm.brp + k + 1) - __ldg(tm.brp + k);
+        }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) n += __shfl_xor_sync(0xffffffffu, n, off);
+    if (lane == 0) cnt[w] = n;
+  }
+}
+
+// warp per row; products written at off[row] + running index, in
+// enumeration order (lanes stride a B row; the A entries and terms advance
+// uniformly)
+template <typename T>
+__global__ void k_det_expand(uint32_t r0, uint32_t rows, const TermDev<T>* terms, int nterms,
+                             const uint64_t* off, uint64_t* keys, AB<T>* ab) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < rows;
+       w += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t r = r0 + w;
+    uint64_t o = off[w];
+    for (int t = 0; t < nterms; ++t) {
+      const TermDev<T> tm = terms[t];
+      const bool ident = tm.arp == nullptr;
+      const uint32_t s0 = ident ? 0u : __ldg(tm.arp + r), s1 = ident ? 1u : __ldg(tm.arp + r + 1);
+      for (uint32_t e = s0; e < s1; ++e) {
+        const uint32_t k = ident ? r : __ldg(tm.aci + e);
+        const T a = ident ? T(1) : __ldg(tm.av + e);
+        const uint32_t bs = __ldg(tm.brp + k), be = __ldg(tm.brp + k + 1);
+        for (uint32_t q = bs + lane; q < be; q += 32) {
+          const uint64_t pos = o + (q - bs);
+          keys[pos] = (uint64_t(w) << 40) | (uint64_t(__ldg(tm.bci + q)) << 8) | uint64_t(t);
+          ab[pos] = AB<T>{a, __ldg(tm.bv + q)};
+        }
+        o += be - bs;
+      }
+    }
+  }
+}
+
+// one thread per (row, col) run of the sorted products: fold the run
+__global__ void k_det_heads(const uint64_t* keys, uint64_t n, uint32_t* head) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    head[i] = (i == 0 || (keys[i] >> 8) != (keys[i - 1] >> 8)) ? 1u : 0u;
+}
+
+template <typename T>
+__global__ void k_det_fold(const uint64_t* keys, const AB<T>* ab, uint64_t n,
+                           const uint32_t* head, const uint32_t* hpos, const TermDev<T>* terms,
+                           uint64_t cbase, uint32_t* cci, T* cv) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    if (!head[i]) continue;
+    const uint64_t rc = keys[i] >> 8;
+    T acc = T(0);
+    bool have = false;
+    uint64_t j = i;
+    while (j < n && (keys[j] >> 8) == rc) {
+      const int t = int(keys[j] & 0xff);
+      const bool ident = terms[t].arp == nullptr;
+      T tsum;
+      if (ident) {
+        tsum = ab[j].b;  // the identity term's value as-is (keeps -0.0)
+        ++j;
+      } else {
+        tsum = T(0);
+        while (j < n && keys[j] == ((rc << 8) | uint64_t(t))) {
+          tsum = fma(ab[j].a, ab[j].b, tsum);
+          ++j;
+        }
+      }
+      acc = have ? acc + tsum : tsum;
+      have = true;
+    }
+    const uint64_t o = cbase + hpos[i];
+    cci[o] = uint32_t(rc & 0xffffffffu);
+    cv[o] = acc;
+  }
+}
+
 // Plan workspace: grow-only stream-ordered scratch per (device, stream,
 // slot) (common.cuh), so repeated products on one stream allocate nothing.
 // A stream has at most one SpGEMM plan in flight (symbolic -> numeric).
@@ -1150,6 +1263,99 @@ int numeric_impl(rdmm_spgemm_plan* P, uint32_t* cci, T* cv, cudaStream_t s) {
   return RDMM_OK;
 }
 
+// Deterministic numeric pass (see k_det_expand): rows in batches of at most
+// kDetBatch products, each expanded, stably sorted and folded.
+constexpr uint64_t kDetBatch = uint64_t(1) << 26;
+
+template <typename T>
+int numeric_det_impl(rdmm_spgemm_plan* P, uint32_t* cci, T* cv, cudaStream_t s) {
+  if (P->nnz == 0) return RDMM_OK;
+  if (!P->c_row_ptr)
+    return fail(RDMM_ERR_INVALID, "spgemm numeric: plan has no row_ptr");
+  if (P->nterms > 255) return fail(RDMM_ERR_INVALID, "spgemm deterministic: at most 255 terms");
+  KernelTimer timer(s, 2);
+  const TermDev<T>* td = P->terms.as<TermDev<T>>();
+  const uint32_t rows = P->rows;
+  // products per row -> host prefix (batch boundaries)
+  uint64_t* cnt = nullptr;
+  RDMM_CUDA_TRY(cudaMallocAsync(&cnt, (size_t(rows) + 1) * 8, s));
+  const unsigned nb = unsigned(std::min<uint64_t>(ceil_div(uint64_t(rows) * 32, 256),
+                                                  uint64_t(num_sms()) * 16));
+  count_launch();
+  k_det_count<T><<<std::max(1u, nb), 256, 0, s>>>(0, rows, td, P->nterms, cnt);
+  std::vector<uint64_t> hc(rows);
+  RDMM_CUDA_TRY(cudaMemcpyAsync(hc.data(), cnt, size_t(rows) * 8, cudaMemcpyDeviceToHost, s));
+  std::vector<uint32_t> rp(size_t(rows) + 1);
+  RDMM_CUDA_TRY(cudaMemcpyAsync(rp.data(), P->c_row_ptr, (size_t(rows) + 1) * 4,
+                                cudaMemcpyDeviceToHost, s));
+  RDMM_CUDA_TRY(cudaStreamSynchronize(s));
+  uint64_t maxb = 0;
+  for (uint64_t x : hc) maxb = std::max(maxb, x);
+  const uint64_t cap = std::max<uint64_t>(std::min<uint64_t>(kDetBatch, std::accumulate(
+                                              hc.begin(), hc.end(), uint64_t(0))), maxb);
+  uint64_t *keys = nullptr, *keys2 = nullptr, *off = nullptr;
+  AB<T>*ab = nullptr, *ab2 = nullptr;
+  uint32_t *head = nullptr, *hpos = nullptr;
+  RDMM_CUDA_TRY(cudaMallocAsync(&keys, cap * 8, s));
+  RDMM_CUDA_TRY(cudaMallocAsync(&keys2, cap * 8, s));
+  RDMM_CUDA_TRY(cudaMallocAsync(&ab, cap * sizeof(AB<T>), s));
+  RDMM_CUDA_TRY(cudaMallocAsync(&ab2, cap * sizeof(AB<T>), s));
+  RDMM_CUDA_TRY(cudaMallocAsync(&head, cap * 4, s));
+  RDMM_CUDA_TRY(cudaMallocAsync(&hpos, cap * 4, s));
+  RDMM_CUDA_TRY(cudaMallocAsync(&off, (size_t(rows) + 1) * 8, s));
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  {
+    size_t a = 0, b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, keys, keys2, ab, ab2, int64_t(cap), 0, 64, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, b, head, hpos, int64_t(cap), s);
+    tmp_bytes = std::max(a, b);
+  }
+  RDMM_CUDA_TRY(cudaMallocAsync(&tmp, std::max<size_t>(tmp_bytes, 16), s));
+  int key_bits = 8;
+  while (key_bits < 40 && (uint64_t(1) << (key_bits - 8)) < uint64_t(P->ncols)) ++key_bits;
+  int rc = RDMM_OK;
+  for (uint32_t r0 = 0; r0 < rows && rc == RDMM_OK;) {
+    uint32_t r1 = r0;
+    uint64_t n = 0;
+    std::vector<uint64_t> ho;
+    while (r1 < rows && (r1 == r0 || n + hc[r1] <= cap) && r1 - r0 < (1u << 23)) {
+      ho.push_back(n);
+      n += hc[r1++];
+    }
+    ho.push_back(n);
+    if (n) {
+      RDMM_CUDA_TRY(cudaMemcpyAsync(off, ho.data(), ho.size() * 8, cudaMemcpyHostToDevice, s));
+      const uint32_t br = r1 - r0;
+      const unsigned eb = unsigned(std::min<uint64_t>(ceil_div(uint64_t(br) * 32, 256),
+                                                      uint64_t(num_sms()) * 16));
+      count_launch(4);
+      k_det_expand<T><<<std::max(1u, eb), 256, 0, s>>>(r0, br, td, P->nterms, off, keys, ab);
+      // row bits above the column and term bits
+      int rbits = 1;
+      while (rbits < 24 && (uint64_t(1) << rbits) < br) ++rbits;
+      size_t tb = tmp_bytes;
+      RDMM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, ab, ab2, int64_t(n), 0,
+                                                    40 + rbits, s));
+      const unsigned fb = unsigned(std::min<uint64_t>(ceil_div(n, 256), uint64_t(num_sms()) * 16));
+      k_det_heads<<<fb, 256, 0, s>>>(keys2, n, head);
+      tb = tmp_bytes;
+      RDMM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, head, hpos, int64_t(n), s));
+      k_det_fold<T><<<fb, 256, 0, s>>>(keys2, ab2, n, head, hpos, td, rp[r0], cci, cv);
+      RDMM_CUDA_TRY(cudaGetLastError());
+      (void)key_bits;
+    }
+    RDMM_CUDA_TRY(cudaStreamSynchronize(s));  // `ho` / offsets reused next batch
+    r0 = r1;
+  }
+  for (void* p : {static_cast<void*>(cnt), static_cast<void*>(keys), static_cast<void*>(keys2),
+                  static_cast<void*>(ab), static_cast<void*>(ab2), static_cast<void*>(head),
+                  static_cast<void*>(hpos), static_cast<void*>(off), tmp})
+    cudaFreeAsync(p, s);
+  RDMM_CUDA_TRY(cudaGetLastError());
+  return rc;
+}
+
 }  // namespace
 
 extern "C" int rdmm_spgemm_symbolic(uint32_t rows, uint32_t ncols,
@@ -1177,6 +1383,18 @@ extern "C" int rdmm_spgemm_numeric(rdmm_spgemm_plan* plan, uint32_t* c_col_idx,
                                     as_stream(stream))
              : numeric_impl<float>(plan, c_col_idx, static_cast<float*>(c_val),
                                    as_stream(stream));
+}
+
+extern "C" int rdmm_spgemm_numeric_ex(rdmm_spgemm_plan* plan, uint32_t* c_col_idx,
+                                      void* c_val, unsigned flags, rdmm_stream_t stream) {
+  if (!plan) return fail(RDMM_ERR_INVALID, "spgemm: null plan");
+  if (!(flags & RDMM_SPGEMM_DETERMINISTIC))
+    return rdmm_spgemm_numeric(plan, c_col_idx, c_val, stream);
+  return plan->dtype == 8
+             ? numeric_det_impl<double>(plan, c_col_idx, static_cast<double*>(c_val),
+                                        as_stream(stream))
+             : numeric_det_impl<float>(plan, c_col_idx, static_cast<float*>(c_val),
+                                       as_stream(stream));
 }
 
 extern "C" void rdmm_spgemm_plan_destroy(rdmm_spgemm_plan* plan) { delete plan; }

@@ -117,9 +117,11 @@ def spmm_local(a: DeviceCsr, b: torch.Tensor, c: torch.Tensor, stream=None,
 
 
 def spgemm_terms(rows: int, ncols: int, terms, dtype=torch.float32, device="cuda",
-                 stream=None, info: dict | None = None):
+                 stream=None, info: dict | None = None, deterministic: bool = False):
     """C = sum_t A_t @ B_t over (A_t | None, B_t) pairs (None = identity),
-    sorted rows, cancelled zeros kept.  Returns (DeviceCsr, FlopMeter)."""
+    sorted rows, cancelled zeros kept.  Returns (DeviceCsr, FlopMeter).
+    deterministic=True: values bitwise equal to the reference's (fma chain in
+    its loop order, terms folded like successive csr_adds) for any inputs."""
     arr = (L.SpgemmTerm * max(1, len(terms)))()
     for i, (a, b) in enumerate(terms):
         if a is not None:
@@ -139,8 +141,9 @@ def spgemm_terms(rows: int, ncols: int, terms, dtype=torch.float32, device="cuda
         out = DeviceCsr.empty(rows, ncols, nnz.value, dtype=dtype, device=device)
         out.row_ptr = rp
         if nnz.value:
-            L.check(L.rdmm_spgemm_numeric(plan, out.col_idx.data_ptr(), out.values.data_ptr(),
-                                          _stream(stream)), "spgemm numeric")
+            L.check(L.rdmm_spgemm_numeric_ex(plan, out.col_idx.data_ptr(), out.values.data_ptr(),
+                                             L.SPGEMM_DETERMINISTIC if deterministic else 0,
+                                             _stream(stream)), "spgemm numeric")
         if info is not None:
             st, nt = (C.c_uint32 * 6)(), (C.c_uint32 * 6)()
             L.rdmm_spgemm_plan_info(plan, st, nt)
@@ -150,12 +153,12 @@ def spgemm_terms(rows: int, ncols: int, terms, dtype=torch.float32, device="cuda
     return out, FlopMeter(fl.value, nnz.value)
 
 
-def spgemm_local(a: DeviceCsr, b: DeviceCsr, stream=None, info=None):
+def spgemm_local(a: DeviceCsr, b: DeviceCsr, stream=None, info=None, deterministic=False):
     """(a @ b, FlopMeter) -- tile.hpp:211-255; DimensionError like :216-217."""
     if a.cols != b.rows:
         raise L.DimensionError("spgemm_local: dimension mismatch")
     return spgemm_terms(a.rows, b.cols, [(a, b)], dtype=a.dtype, device=a.device,
-                        stream=stream, info=info)
+                        stream=stream, info=info, deterministic=deterministic)
 
 
 def csr_add(a: DeviceCsr, b: DeviceCsr, stream=None) -> DeviceCsr:

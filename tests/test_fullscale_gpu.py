@@ -182,3 +182,35 @@ def test_multi_gpu_bench_layouts_verify(gpus, args):
     d = _bench(args, gpus)
     assert d["n_gpus"] == gpus
     assert d["verify"]["ok"], d["verify"]
+
+
+def test_distributed_spgemm_deterministic_real_values():
+    """stationary-C SpGEMM with RunOptions::deterministic on real values: two
+    runs bitwise identical, values within the fp32 gate of the fp64 oracle."""
+    import paper_2311_18141_b200.dist as dist
+
+    orc = oracle.port()
+    h = orc.rmat(12, 8, seed=2)
+    h.values = oracle.real_twin(h.nnz, 7, np.float32)
+    h64 = oracle.Csr(h.rows, h.cols, h.row_ptr, h.col_idx, h.values.astype(np.float64))
+    want, _ = orc.spgemm_local(h64, h64)
+    habs = oracle.Csr(h.rows, h.cols, h.row_ptr, h.col_idx, np.abs(h64.values))
+    bound, _ = orc.spgemm_local(habs, habs)
+    outs = []
+    for _ in range(2):
+        with dist.Fabric(nranks=4, heap_bytes=256 << 20,
+                         devices=[r % torch.cuda.device_count() for r in range(4)]) as f:
+            g = dist.ProcGrid(2, 2)
+            t = -(-h.rows // 4)
+            A = dist.DistSparse(f, h.rows, h.cols, t, t, g, 0)
+            B = dist.DistSparse(f, h.rows, h.cols, t, t, g, 1)
+            Cm = dist.DistSparse(f, h.rows, h.cols, t, t, g, 2)
+            A.init_from_global(h.row_ptr, h.col_idx, h.values)
+            B.init_from_global(h.row_ptr, h.col_idx, h.values)
+            Cm.init()
+            dist.run_multiply(f, A, B, Cm, variant="stationary_c", deterministic=True)
+            outs.append(Cm.to_global())
+    (rp1, ci1, v1), (rp2, ci2, v2) = outs
+    assert np.array_equal(rp1, want.row_ptr) and np.array_equal(ci1, want.col_idx)
+    assert np.array_equal(v1.view(np.uint32), v2.view(np.uint32))
+    assert np.all(np.abs(v1.astype(np.float64) - want.values) <= 1e-5 * bound.values + 1e-30)

@@ -209,3 +209,42 @@ def test_cfg4_full_scale_property(rd):
     starts = torch.zeros(c.nnz, dtype=torch.bool, device=DEV)
     starts[c.row_ptr.long()[1:-1].clamp(max=c.nnz - 1)] = True
     assert bool(torch.all(inc | starts[1:]))
+
+
+@pytest.mark.parametrize("dt,tag", [(np.float32, "f32"), (np.float64, "f64")])
+def test_deterministic_values_equal_reference_bitwise(rd, golden, dt, tag):
+    """RDMM_SPGEMM_DETERMINISTIC: real-valued A*A bitwise equal to the
+    reference's own result (golden from oracle/_ref, tile.hpp:211-255)."""
+    a9 = oracle.port().rmat(9, 8, seed=1)
+    ar = oracle.Csr(a9.rows, a9.cols, a9.row_ptr, a9.col_idx, oracle.real_twin(a9.nnz, 3, dt))
+    c, _ = rd.spgemm_local(dev(rd, ar), dev(rd, ar), deterministic=True)
+    got = host(c)
+    same_structure(got, oracle.Csr(a9.rows, a9.cols, golden["spgemm9_rp"],
+                                   golden["spgemm9_ci"], golden["spgemm9_v"]))
+    assert np.array_equal(got.values, golden["spgemm9_real_v_" + tag])
+
+
+def test_deterministic_matches_oracle_fma_chain_rmat14(rd, orc):
+    """Larger R-MAT (every hash tier and the dense tier's rows): bitwise equal
+    to the oracle's fma chain, and identical run to run."""
+    h = orc.rmat(14, 8, seed=3)
+    h.values = oracle.real_twin(h.nnz, 5, np.float32)
+    want, _ = orc.spgemm_local(h, h)
+    c1, _ = rd.spgemm_local(dev(rd, h), dev(rd, h), deterministic=True)
+    c2, _ = rd.spgemm_local(dev(rd, h), dev(rd, h), deterministic=True)
+    g1, g2 = host(c1), host(c2)
+    exact(g1, want)
+    assert np.array_equal(g1.values.view(np.uint32), g2.values.view(np.uint32))
+
+
+def test_deterministic_csr_add_keeps_signed_zeros(rd):
+    x = oracle.Csr(2, 3, np.array([0, 2, 3], np.uint32), np.array([0, 2, 1], np.uint32),
+                   np.array([-0.0, 1.5, 2.0], np.float32))
+    y = oracle.Csr(2, 3, np.array([0, 1, 2], np.uint32), np.array([1, 1], np.uint32),
+                   np.array([-0.0, -2.0], np.float32))
+    out, _ = rd.spgemm_terms(2, 3, [(None, dev(rd, x)), (None, dev(rd, y))],
+                             deterministic=True)
+    got = host(out)
+    assert np.array_equal(got.col_idx, [0, 1, 2, 1])
+    assert np.array_equal(got.values, np.array([-0.0, -0.0, 1.5, 0.0], np.float32))
+    assert np.signbit(got.values[0]) and np.signbit(got.values[1]) and not np.signbit(got.values[3])
