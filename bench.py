@@ -454,7 +454,7 @@ def run_ours(args, cfg, dev, rank, world):
                 cols = min(n, (j + 1) * tn) - j * tn
                 nnz_i = int(rp_host[r1]) - int(rp_host[r0])
                 alg += 4 * (r1 - r0 + 1) * ktiles + 8 * nnz_i + 4 * k * cols + 4 * (r1 - r0) * cols
-        kernel = "spmm_stream+spmm_fixup (rdmm_spmm_csr), all launches of a step on this rank"
+        kernel = "spmm_stream_full|spmm_stream|spmm_slots_async + spmm_fixup (rdmm_spmm_csr), all launches of a step on this rank"
     else:
         alg = (2 * a_bytes + (m + 1) * 4 + 8 * (out_nnz or 0)) // world
         kernel = ("spgemm symbolic + numeric passes (rdmm_spgemm_symbolic/numeric), per step "

@@ -148,6 +148,9 @@ struct SpmmArgs {
   // pieces of rows cut by chunk boundaries, is a red.global.add into C; no
   // C read, no head/tail fix-up, products of several launches may overlap
   int atomic;
+  // spmm_stream_full may run: rows of exactly 32 16-byte vectors, one
+  // contiguous B, B/C vector indices and chunk positions within 32 bits
+  int full_ok;
   uint64_t ldb, ldc;
   uint64_t nnz, Q;
   uint32_t rows, nvec, nchunks, wstride;
@@ -397,6 +400,115 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (lane == 0) p.tail_row[c] = trow;
   }
 }
+
+
+// spmm_stream_full: the stream crossed the end of `row` at position pos --
+// store it (or park it in the head slot when the chunk started inside it)
+// and move to the row holding pos (skipping empty rows).
+template <typename T, bool CZERO, typename V>
+__device__ __forceinline__ void stream_next_row(const SpmmArgs<T>& p, V* __restrict__ Cl,
+                                                uint32_t ldcv, uint32_t head_idx, uint32_t pos,
+                                                uint32_t lane, uint32_t& rb, uint32_t& row,
+                                                uint32_t& rew, uint32_t& rend, bool& starts,
+                                                V& acc) {
+  if (starts) __stcs(Cl + row * ldcv, acc);
+  else reinterpret_cast<V*>(p.head_val)[head_idx] = acc;
+  for (;;) {
+    const uint32_t d = __popc(__ballot_sync(0xffffffffu, rew <= pos));
+    if (d < 32u) {
+      row = rb + d;
+      rend = __shfl_sync(0xffffffffu, rew, d);
+      break;
+    }
+    rb += 32;
+    rew = rb + lane < p.rows ? __ldg(p.rp + rb + lane + 1) : 0xFFFFFFFFu;
+  }
+  starts = true;
+  acc = CZERO ? vzero<V>() : __ldcs(Cl + row * ldcv);
+}
+
+
+// spmm_stream for the headline shape (rows of exactly 32 16-byte vectors:
+// N = 128 fp32 / 64 fp64, one contiguous B): the same nnz-chunk stream with
+// the per-nonzero instruction count cut from ~30 to ~10 -- every lane holds
+// its window entry's B row offset (k * ldb, 32-bit) so a gather is one
+// shuffle + one IMAD.WIDE + one LDG, positions are 32-bit, a full window
+// (32 nonzeros) runs without bounds checks and no lane is masked.
+template <typename T, bool CZERO>
+__global__ void __launch_bounds__(kThreads, 4) spmm_stream_full(const SpmmArgs<T> p) {
+  constexpr int VEC = 16 / sizeof(T);
+  using V = typename VecOf<T, VEC>::type;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int U = 8;  // gathers in flight per lane
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = gridDim.x * (kThreads / 32);
+  const V* __restrict__ Bl = reinterpret_cast<const V*>(p.B) + lane;
+  V* __restrict__ Cl = reinterpret_cast<V*>(p.C) + lane;
+  const uint32_t ldbv = uint32_t(p.ldb / VEC), ldcv = uint32_t(p.ldc / VEC);
+  const uint32_t nnz = uint32_t(p.nnz), Q = uint32_t(p.Q);
+  const uint32_t wsv = p.wstride / VEC;
+
+  for (uint32_t c = warp; c < p.nchunks; c += nwarps) {
+    const uint32_t lo = c * Q;
+    const uint32_t hi = min(lo + Q, nnz);
+    uint32_t rb = __ldg(p.chunk_row + c), row = rb;
+    uint32_t rew = rb + lane < p.rows ? __ldg(p.rp + rb + lane + 1) : 0xFFFFFFFFu;
+    bool starts = __ldg(p.rp + row) >= lo;
+    uint32_t rend = __shfl_sync(FULL, rew, 0);
+    V acc = (!CZERO && starts) ? __ldcs(Cl + row * ldcv) : vzero<V>();
+    uint32_t off;
+    T a;
+    {
+      const uint32_t idx = lo + lane;
+      const bool ok = idx < hi;
+      off = (ok ? __ldcs(p.ci + idx) : 0u) * ldbv;
+      a = ok ? __ldcs(p.val + idx) : T(0);
+    }
+    for (uint32_t w = lo; w < hi; w += 32) {
+      uint32_t kn;
+      T an;
+      {
+        const uint32_t idx = w + 32 + lane;
+        const bool ok = idx < hi;
+        kn = ok ? __ldcs(p.ci + idx) : 0u;
+        an = ok ? __ldcs(p.val + idx) : T(0);
+      }
+      // a partial last window gathers row 0 for its missing entries (off =
+      // 0) and skips them: one code path, no per-gather bounds checks
+#pragma unroll 1
+      for (int t = 0; t < 32; t += U) {
+        V bv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) bv[u] = __ldg(Bl + __shfl_sync(FULL, off, t + u));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const T au = __shfl_sync(FULL, a, t + u);
+          const uint32_t pos = w + t + u;
+          if (pos < hi) {
+            if (pos >= rend)
+              stream_next_row<T, CZERO>(p, Cl, ldcv, c * wsv + lane, pos, lane, rb, row, rew,
+                                        rend, starts, acc);
+            acc = vfma(au, bv[u], acc);
+          }
+        }
+      }
+      off = kn * ldbv;
+      a = an;
+    }
+    // the chunk's last row
+    int32_t trow = -1;
+    if (rend <= hi && starts) {
+      __stcs(Cl + row * ldcv, acc);
+    } else {
+      reinterpret_cast<V*>(starts ? p.tail_val : p.head_val)[c * wsv + lane] = acc;
+      if (starts) trow = int32_t(row);
+    }
+    if (lane == 0) p.tail_row[c] = trow;
+  }
+}
+
+
 
 
 // Chunking of a launch: nnz, chunk length Q and chunk count, from the host
@@ -1261,6 +1373,15 @@ inline bool async_mode() {
   return v;
 }
 
+// RDMM_SPMM_FULL=0 disables spmm_stream_full (a measurement switch).
+inline bool full_mode() {
+  static const bool v = [] {
+    const char* e = std::getenv("RDMM_SPMM_FULL");
+    return !(e && std::string(e) == "0");
+  }();
+  return v;
+}
+
 // Kernel choice, measured on B200 (profiles/):
 //  * narrow rows (nvec < 32 vectors: N < 128 fp32) -> spmm_slots, the warp
 //    streaming one nnz chunk with S = 32/L slots (N = 32 on cfg3's A:
@@ -1313,6 +1434,9 @@ void launch_seg(const SpmmArgs<T>& a, bool czero, int blocks, cudaStream_t s) {
     if (use_rows) {
       if (czero) spmm_rows<T, VEC, G, NV, true, MB, SEG><<<blocks, kThreads, 0, s>>>(a);
       else spmm_rows<T, VEC, G, NV, false, MB, SEG><<<blocks, kThreads, 0, s>>>(a);
+    } else if (a.full_ok && !SEG && NV == 1 && G == 32 && VEC * sizeof(T) == 16) {
+      if (czero) spmm_stream_full<T, true><<<blocks, kThreads, 0, s>>>(a);
+      else spmm_stream_full<T, false><<<blocks, kThreads, 0, s>>>(a);
     } else {
       if (czero) spmm_stream<T, VEC, G, NV, true, MB, SEG><<<blocks, kThreads, 0, s>>>(a);
       else spmm_stream<T, VEC, G, NV, false, MB, SEG><<<blocks, kThreads, 0, s>>>(a);
@@ -1524,6 +1648,10 @@ int spmm_impl(uint32_t rows, uint32_t cols, uint32_t n, uint64_t nnz,
   // atomic accumulation: the narrow slot kernels only (others ignore it)
   a.atomic = (flags & RDMM_SPMM_ATOMIC) != 0 && narrow_slots;
   const uint32_t nvec_total = n / P.VEC;
+  a.full_ok = full_mode() && !nseg && P.VEC == VV && nvec_total == 32 &&
+              (kernel_variant() == 0 || kernel_variant() == 2) &&
+              uint64_t(cols) * (ldb / VV) < (1ull << 32) &&
+              uint64_t(rows) * (ldc / VV) < (1ull << 32) && nnz + P.Q < (1ull << 32);
   KernelTimer timer(s, 1);
   count_launch(1);
   spmm_chunk_rows<<<P.chunk_blocks, kThreads, 0, s>>>(rp, rows, P.Q, P.nchunks, chunk_row,
