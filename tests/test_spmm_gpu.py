@@ -178,3 +178,39 @@ def test_cfg3_full_scale_property(rd):
     c2 = torch.zeros_like(c)
     rd.spmm_local(a, b, c2)
     assert torch.equal(c, c2)
+
+
+def _hub_csr(rows, cols, seed, dtype):
+    """Short random rows, empty rows, and a few hub rows with every column:
+    the hub rows span many nnz chunks (head/tail fix-ups), the empty rows
+    are skipped by the row window, partial last windows everywhere."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, 6, rows)
+    lens[rng.random(rows) < 0.4] = 0
+    for r in (0, 7, rows // 2, rows - 1):
+        lens[r] = cols
+    rp = np.zeros(rows + 1, np.uint32)
+    rp[1:] = np.cumsum(lens)
+    ci = np.concatenate([np.arange(cols, dtype=np.uint32) if n == cols else
+                         np.sort(rng.choice(cols, n, replace=False)).astype(np.uint32)
+                         for n in lens])
+    vals = rng.integers(-3, 4, ci.size).astype(dtype)
+    return oracle.Csr(rows, cols, rp, ci, vals)
+
+
+@pytest.mark.parametrize("dt,n", [(np.float32, 128), (np.float64, 64)])
+@pytest.mark.parametrize("rows", [5, 3000])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_full_row_stream_edges(rd, orc, dt, n, rows, accumulate):
+    """spmm_stream_full (rows of 32 16-byte vectors): hub rows cut by chunks,
+    empty rows, partial windows, C-zero and accumulate forms, bit-exact."""
+    h = _hub_csr(rows, 2048, rows + n, dt)
+    b = orc.random_dense(h.cols, n, 3, dtype=dt)
+    c0 = orc.random_dense(h.rows, n, 4, dtype=dt) if accumulate else np.zeros((h.rows, n), dt)
+    want = c0.copy()
+    orc.spmm_local(h, b, want)
+    a = dev_csr(rd, h)
+    ct = torch.from_numpy(c0.copy()).to(DEV)
+    rd.spmm_local(a, torch.from_numpy(b).to(DEV), ct, c_zero=not accumulate)
+    torch.cuda.synchronize()
+    assert np.array_equal(ct.cpu().numpy(), want)
