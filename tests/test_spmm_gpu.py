@@ -187,8 +187,9 @@ def _hub_csr(rows, cols, seed, dtype):
     rng = np.random.default_rng(seed)
     lens = rng.integers(0, 6, rows)
     lens[rng.random(rows) < 0.4] = 0
-    for r in (0, 7, rows // 2, rows - 1):
-        lens[r] = cols
+    for r in {0, 7, rows // 2, rows - 1}:
+        if r < rows:
+            lens[r] = cols
     rp = np.zeros(rows + 1, np.uint32)
     rp[1:] = np.cumsum(lens)
     ci = np.concatenate([np.arange(cols, dtype=np.uint32) if n == cols else
