@@ -536,15 +536,15 @@ __global__ void __launch_bounds__(G == 32 ? 256 : G)
 // The symbolic pass keeps the whole bitmap in shared memory when it fits.
 constexpr int kWc = 8192;  // write-combining slots per CTA
 
-template <typename T>
+template <typename T, int WC = kWc>
 constexpr size_t dense_smem_bytes() {
-  return size_t(kWc) * (4 + sizeof(T));
+  return size_t(WC) * (4 + sizeof(T));
 }
 
 // SBM: the row's column bitmap lives in shared memory after the
 // write-combining cache (CL = 1 and ncols <= ~1M fp32): the bitmap atomics,
 // the count scan and the emission scan never touch HBM.
-template <typename T, int CL, bool SBM>
+template <typename T, int CL, bool SBM, int WC = kWc>
 __global__ void __launch_bounds__(kDenseThreads)
     k_dense_num(const uint32_t* __restrict__ list, uint32_t count,
                 const TermDev<T>* terms, int nterms,
@@ -552,18 +552,18 @@ __global__ void __launch_bounds__(kDenseThreads)
                 T* __restrict__ cv, uint32_t* bitmaps, T* dense, uint32_t nwords,
                 uint32_t ncols, T ident_val, int flat) {
   constexpr int G = kDenseThreads;
-  constexpr int LOG2W = __builtin_ctz(kWc);
+  constexpr int LOG2W = __builtin_ctz(WC);
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char dsm[];
   uint32_t* wkey = reinterpret_cast<uint32_t*>(dsm);
-  T* wval = reinterpret_cast<T*>(dsm + size_t(kWc) * 4);
+  T* wval = reinterpret_cast<T*>(dsm + size_t(WC) * 4);
   __shared__ Win<T, G> win;
   __shared__ uint32_t slice_count;
   __shared__ uint32_t coff[G];  // emission: output offset of each 32-word chunk
   const uint32_t part = CL > 1 ? cluster.block_rank() : 0;
   const uint32_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
-  uint32_t* bm = SBM ? reinterpret_cast<uint32_t*>(dsm + dense_smem_bytes<T>())
+  uint32_t* bm = SBM ? reinterpret_cast<uint32_t*>(dsm + dense_smem_bytes<T, WC>())
                      : bitmaps + size_t(cid) * nwords;
   auto ldbm = [&](uint32_t w) -> uint32_t {
     if constexpr (SBM) return reinterpret_cast<volatile uint32_t*>(bm)[w];
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(kDenseThreads)
   const uint32_t wper = (nwords + CL - 1) / CL;
   const uint32_t ws0 = min(part * wper, nwords), ws1 = min(ws0 + wper, nwords);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t i = threadIdx.x; i < kWc; i += G) {
+  for (uint32_t i = threadIdx.x; i < WC; i += G) {
     wkey[i] = kEmpty;
     wval[i] = ident_val;
   }
@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(kDenseThreads)
     // CTAs' caches overlap; flush them into the dense array.
     __syncthreads();
     if constexpr (CL > 1) {
-      for (uint32_t i = threadIdx.x; i < kWc; i += G) {
+      for (uint32_t i = threadIdx.x; i < WC; i += G) {
         const uint32_t key = wkey[i];
         if (key != kEmpty) {
           atomicAdd(dv + key, wval[i]);
@@ -693,7 +693,7 @@ __global__ void __launch_bounds__(kDenseThreads)
       run += total;
       __syncthreads();
     }
-    for (uint32_t i = threadIdx.x; i < kWc; i += G) {  // reset the cache
+    for (uint32_t i = threadIdx.x; i < WC; i += G) {  // reset the cache
       wkey[i] = kEmpty;
       wval[i] = ident_val;
     }
@@ -839,9 +839,20 @@ int launch_dense_num(uint32_t slots, const uint32_t* list, uint32_t count,
                      cudaStream_t s) {
   // static shared memory of the kernel: Win<T, G> + a counter
   const size_t stat = sizeof(Win<T, kDenseThreads>) + 64 + kDenseThreads * 4;
-  const bool sbm = CL == 1 && dense_smem_bytes<T>() + size_t(nwords) * 4 + stat <= 226 * 1024;
-  auto fn = sbm ? k_dense_num<T, CL, true> : k_dense_num<T, CL, false>;
-  const size_t sm = dense_smem_bytes<T>() + (sbm ? size_t(nwords) * 4 : 0);
+  // 16384 write-combining slots (the bitmap then lives in global memory /
+  // L2): cfg4 s20 132.8 -> 129.7 ms against 8192 slots with the bitmap in
+  // shared memory.  RDMM_SPGEMM_WC=8192 restores the latter (a measurement
+  // switch).
+  static const int wc_env = [] {
+    const char* e = std::getenv("RDMM_SPGEMM_WC");
+    return e ? std::atoi(e) : 0;
+  }();
+  const bool big = wc_env != kWc;
+  const size_t wcb = big ? dense_smem_bytes<T, 2 * kWc>() : dense_smem_bytes<T>();
+  const bool sbm = CL == 1 && wcb + size_t(nwords) * 4 + stat <= 226 * 1024;
+  auto fn = big ? (sbm ? k_dense_num<T, CL, true, 2 * kWc> : k_dense_num<T, CL, false, 2 * kWc>)
+                : (sbm ? k_dense_num<T, CL, true> : k_dense_num<T, CL, false>);
+  const size_t sm = wcb + (sbm ? size_t(nwords) * 4 : 0);
   RDMM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(slots * CL);
