@@ -1491,10 +1491,18 @@ constexpr int kMaxNV = 4;
 // Panel width in vectors handled by one launch pair.
 inline uint32_t panel_vecs() { return 32u * kMaxNV; }
 
-inline uint32_t chunk_count(uint64_t nnz, uint32_t workers) {
-  // ~8 chunks per resident worker for tail smoothing, >= 64 nnz each.
+inline uint32_t chunk_count(uint64_t nnz, uint32_t workers, bool narrow) {
+  // chunks per resident worker for tail smoothing, >= 64 nnz each: 8 for
+  // full-width rows, 16 for the narrow slot kernels (N = 32 on cfg3's A:
+  // 1.120 -> 1.054 ms; N = 128 2.97 -> 2.95).  RDMM_SPMM_CPW overrides (a
+  // measurement switch).
+  static const int env = [] {
+    const char* e = std::getenv("RDMM_SPMM_CPW");
+    return e ? std::atoi(e) : 0;
+  }();
+  const uint64_t cpw = env > 0 ? uint64_t(env) : narrow ? 16u : 8u;
   uint64_t by_size = ceil_div(nnz, 64);
-  uint64_t by_workers = uint64_t(workers) * 8;
+  uint64_t by_workers = uint64_t(workers) * cpw;
   uint64_t n = std::max<uint64_t>(1, std::min(by_size, by_workers));
   return uint32_t(std::min<uint64_t>(n, 1u << 30));
 }
@@ -1547,7 +1555,7 @@ SpmmPlan make_plan(uint32_t rows, uint64_t nnz, uint32_t n, int vmode) {
   const int blocks_max = sms * 8;  // 8 x 256 threads per SM (register bound)
   const uint32_t per_block = kThreads / wl;
   const uint32_t workers = uint32_t(blocks_max) * per_block;
-  const uint32_t nchunks = chunk_count(std::max<uint64_t>(nnz, 1), workers);
+  const uint32_t nchunks = chunk_count(std::max<uint64_t>(nnz, 1), workers, G < 32);
   P.Q = ceil_div(std::max<uint64_t>(nnz, 1), nchunks);
   P.nchunks = uint32_t(ceil_div(std::max<uint64_t>(nnz, 1), P.Q));
   P.wstride = uint32_t(ceil_div(uint64_t(P.pv) * P.VEC, 4) * 4);
