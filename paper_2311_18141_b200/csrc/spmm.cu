@@ -1493,9 +1493,10 @@ inline uint32_t panel_vecs() { return 32u * kMaxNV; }
 
 inline uint32_t chunk_count(uint64_t nnz, uint32_t workers, bool narrow) {
   // chunks per resident worker for tail smoothing, >= 64 nnz each: 8 for
-  // full-width rows, 16 for the narrow slot kernels (N = 32 on cfg3's A:
-  // 1.120 -> 1.054 ms; N = 128 2.97 -> 2.95).  RDMM_SPMM_CPW overrides (a
-  // measurement switch).
+  // full-width rows and rows under 8 vectors, 16 for the narrow slot kernels
+  // of 8-31 vectors (cfg3's A at N = 32: 1.120 -> 1.054 ms, N = 64 1.87 ->
+  // 1.80; N = 16 measured 0.809 at 8 vs 0.836 at 16).  RDMM_SPMM_CPW
+  // overrides (a measurement switch).
   static const int env = [] {
     const char* e = std::getenv("RDMM_SPMM_CPW");
     return e ? std::atoi(e) : 0;
@@ -1555,7 +1556,7 @@ SpmmPlan make_plan(uint32_t rows, uint64_t nnz, uint32_t n, int vmode) {
   const int blocks_max = sms * 8;  // 8 x 256 threads per SM (register bound)
   const uint32_t per_block = kThreads / wl;
   const uint32_t workers = uint32_t(blocks_max) * per_block;
-  const uint32_t nchunks = chunk_count(std::max<uint64_t>(nnz, 1), workers, G < 32);
+  const uint32_t nchunks = chunk_count(std::max<uint64_t>(nnz, 1), workers, G >= 8 && G < 32);
   P.Q = ceil_div(std::max<uint64_t>(nnz, 1), nchunks);
   P.nchunks = uint32_t(ceil_div(std::max<uint64_t>(nnz, 1), P.Q));
   P.wstride = uint32_t(ceil_div(uint64_t(P.pv) * P.VEC, 4) * 4);
